@@ -1,0 +1,149 @@
+// Shared device helpers for the libakv kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+#include "akv.h"
+
+namespace akv {
+
+constexpr int D = AKV_HEAD_DIM;
+constexpr int P = AKV_PAGE_TOKENS;
+constexpr int PAGE = AKV_PAGE_BYTES;
+constexpr int MID = AKV_PAGE_MID_OFF;
+constexpr int LOW = AKV_PAGE_LOW_OFF;
+constexpr int PPC = AKV_PAGES_PER_CTA;
+
+// fp16 pattern helpers -------------------------------------------------------
+__device__ __forceinline__ int bexp16(uint32_t w) { return (w >> 10) & 0x1F; }
+__device__ __forceinline__ bool finite16(uint32_t w) { return (w & 0x7C00u) != 0x7C00u; }
+
+// floor(log2|x|) of a finite non-zero fp16 pattern (HB:108-118, subnormal aware).
+__device__ __forceinline__ int magexp16(uint32_t w) {
+  const int b = bexp16(w);
+  if (b) return b - 15;
+  const uint32_t m = w & 0x3FFu;  // caller guarantees m != 0
+  return (31 - __clz(m)) - 24;
+}
+
+// floor(log2|x|) of a finite non-zero fp32 value (frexp exponent - 1).
+__device__ __forceinline__ int floor_log2f(float x) {
+  const uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
+  const int e = (int)(b >> 23);
+  if (e) return e - 127;
+  return (31 - __clz(b)) - 149;
+}
+
+// Byte permute (PRMT).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Bit select: (a & m) | (b & ~m)  — a single LOP3.
+__device__ __forceinline__ uint32_t bsel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+
+// Assemble the 8 fp16 words of one 8-group from its head bytes (h0: elements
+// 0..3, h1: 4..7) and the group's mid / low words (packing in akv.h).
+// out[k] holds elements (2k, 2k+1) as a half2 bit pattern.
+__device__ __forceinline__ void assemble8(uint32_t h0, uint32_t h1, uint32_t mid, uint32_t low, uint32_t out[4]) {
+  const uint32_t x = bsel(0xF0F0F0F0u, mid, low);              // low bytes of elements 0..3
+  const uint32_t y = bsel(0xF0F0F0F0u, mid << 4, low >> 4);    // low bytes of elements 4..7
+  out[0] = prmt(x, h0, 0x5140);
+  out[1] = prmt(x, h0, 0x7362);
+  out[2] = prmt(y, h1, 0x5140);
+  out[3] = prmt(y, h1, 0x7362);
+}
+
+// Tier masks: mid' = bsel(mk, mid, 0x88888888); low' = bsel(lk, low, lf).
+struct TierMask {
+  uint32_t mk, lk, lf;
+};
+__device__ __forceinline__ TierMask tier_mask(int code) {
+  TierMask t;
+  t.mk = code >= 12 ? 0xFFFFFFFFu : 0u;
+  t.lk = code >= 16 ? 0xFFFFFFFFu : 0u;
+  t.lf = code == 12 ? 0x88888888u : 0u;
+  return t;
+}
+
+// Streaming global loads: read-only, no L1 allocation, L2 evict-first policy
+// (the KV planes are read once per step; keep L2 for scores / probs).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint2 ld_stream_u64(const void* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const void* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+__device__ __forceinline__ float2 half2_bits_to_float2(uint32_t w) {
+  __half2 h = *reinterpret_cast<__half2*>(&w);
+  return __half22float2(h);
+}
+
+// acc(x,y) += p * (v.x, v.y) via the packed FFMA2.
+__device__ __forceinline__ float2 ffma2_scalar(float2 v, float p, float2 acc) {
+  float2 r;
+  const float2 pp = make_float2(p, p);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&v)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&pp)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&acc)));
+  return r;
+}
+
+// Warp reductions.
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ long long status_word(long long code, long long pos) { return (code << 60) | pos; }
+
+__device__ __forceinline__ const uint8_t* page_ptr(const uint8_t* pool, const int32_t* table, int max_pages, int u,
+                                                   int pg) {
+  return pool + (size_t)table[(size_t)u * max_pages + pg] * PAGE;
+}
+
+}  // namespace akv

@@ -1,0 +1,260 @@
+"""GPU (libakv, sm_100a) vs CPU oracle parity — SURVEY §8(c).
+
+Bit-exact: stored planes, ColMax/RowMax, K tier masks, V tier masks (with
+the D11 knife-edge protocol, plus an injection check that must be 100 %
+exact), selection sets, AccessCounter totals.  Within 1e-3 (per vector,
+|gpu-ref| <= 1e-3|ref| + 1e-3 max|ref|): scores and outputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import attention_decode as OA
+from oracle import half_bits as ohb
+from oracle.align_core import AlignConfig as OAlignConfig
+from oracle.analysis import relative_error_histogram
+from oracle.kv_store import PlaneTensor as OPlane
+from paper_2409_16546_b200 import AlignConfig, DegenerateInputError, KVStore
+from paper_2409_16546_b200 import attention_decode as AD
+from tests.gpu_helpers import Case, close
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("n", [1, 7, 255, 256, 257, 600])
+def test_planes_and_sidecars_bitexact(n):
+    c = Case(B=2, Hkv=3, n=n, seed=100 + n)
+    for which, src in (("k", c.K), ("v", c.V)):
+        p0, p1, p2 = c.store.export_planes(which)
+        for u in range(6):
+            b, h = divmod(u, 3)
+            ref = OPlane.from_words(src[u])
+            assert np.array_equal(p0[b, h], ref.plane0)
+            assert np.array_equal(p1[b, h], ref.plane1)
+            assert np.array_equal(p2[b, h], ref.plane2)
+    cm = c.store.colmax().cpu().numpy()
+    rm = c.store.rowmax().cpu().numpy().view(np.uint16)
+    for u in range(6):
+        b, h = divmod(u, 3)
+        o = c.ostore(u)
+        assert np.array_equal(cm[b, h].astype(np.uint16), o.colmax)
+        assert np.array_equal(rm[b, h, :n], o.rowmax)
+    assert (c.store.lengths == n).all()
+
+
+def test_append_rejects_nonfinite_with_position():
+    st = KVStore(1, 2, 128, 512)
+    k = torch.randn(1, 2, 5, 128).half()
+    v = torch.randn(1, 2, 5, 128).half()
+    st.append(k, v)
+    k2 = torch.randn(1, 2, 128).half()
+    v2 = torch.randn(1, 2, 128).half()
+    v2[0, 1, 77] = float("inf")
+    with pytest.raises(ValueError, match=r"non-finite half word 0x7C00 in V at batch 0, kv-head 1, token 5, channel 77"):
+        st.append_token(k2, v2)
+    assert st.lengths.tolist() == [[5, 5]]
+    assert st.lengths_dev.cpu().tolist() == [5, 5]
+    kb = torch.randn(1, 2, 3, 128).half()
+    kb[0, 0, 2, 9] = float("nan")
+    with pytest.raises(ValueError, match=r"in K at batch 0, kv-head 0, token 7, channel 9"):
+        st.append(kb, torch.randn(1, 2, 3, 128).half())
+    assert st.lengths.tolist() == [[5, 5]]
+    st.append_token(k2, torch.randn(1, 2, 128).half())
+    assert st.lengths.tolist() == [[6, 6]]
+
+
+def _compare_case(c: Case, cfg=AlignConfig(), ocfg=OAlignConfig(), strategy="element", force=None,
+                  allow_edges=True):
+    r = c.gpu(cfg=cfg, strategy=strategy, force_tier=force)
+    s = r.scores.cpu().numpy()
+    p = r.probs.cpu().numpy()
+    o = r.o.cpu().numpy()
+    kt = r.k_tiers.cpu().numpy()
+    vt = r.v_tiers.cpu().numpy()
+    cnt = r.counters.cpu().numpy()
+    edges = 0
+    for u, b, hq, j in c.units():
+        ref = c.oracle(u, j, ocfg, strategy=strategy, force_tier=force)
+        assert np.array_equal(kt[b, hq], ref.k_tiers), (u, j)
+        assert close(s[b, hq], ref.s), (u, j, np.abs(s[b, hq] - ref.s).max())
+        assert close(o[b, hq], ref.o), (u, j, np.abs(o[b, hq] - ref.o).max())
+        assert tuple(cnt[b, hq, :3]) == ref.k_counter.as_tuple()
+        sel = r.selection(b, hq)
+        if force is None:
+            rows, cols, edge = OA.knife_edges(ref.p, ref.o_est, ref.sel)
+        else:
+            rows, cols, edge = np.zeros(c.n, bool), np.zeros(128, bool), False
+        if edge:
+            edges += 1
+            continue
+        assert np.array_equal(sel, ref.sel), (u, j)
+        keep = ~rows[:, None] & ~cols[None, :]
+        assert np.array_equal(vt[b, hq][keep], ref.v_tiers[keep]), (u, j)
+        if not rows.any() and not cols.any():
+            assert tuple(cnt[b, hq, 3:6]) == ref.v_counter.as_tuple(), (u, j)
+        # injection: the GPU's own p / sel / targets through the oracle rule -> 100 % exact
+        if force is None and strategy == "element":
+            tg = r.targets[b, hq].cpu().numpy().astype(np.int64)
+            known = tg != -(1 << 31)
+            inj = OA.v_element_codes(p[b, hq].astype(np.float64), sel, tg, known, c.V[u] >> 8,
+                                     ocfg)
+            assert np.array_equal(vt[b, hq], inj), (u, j)
+    assert allow_edges or edges == 0
+    return r
+
+
+@pytest.mark.parametrize("n", [16, 256, 1000])
+def test_mha_parity(n):
+    _compare_case(Case(B=2, Hkv=2, g=1, n=n, seed=n))
+
+
+@pytest.mark.parametrize("g", [2, 4, 8])
+def test_gqa_parity(g):
+    _compare_case(Case(B=1, Hkv=2, g=g, n=513, seed=40 + g))
+
+
+def test_flat_scales_parity():
+    """Paper-like regime (U[-0.5,0.5]): many T12/T16 reads and element-path V rows."""
+    c = Case(B=2, Hkv=2, g=2, n=700, seed=5, lo=-0.5, hi=0.5)
+    r = _compare_case(c)
+    st = r.v_stats()
+    assert st.t12 + st.t16 > st.elements_read * 0.001
+
+
+@pytest.mark.parametrize("margin,zero_skip", [(-2, True), (4, True), (0, False)])
+def test_config_parity(margin, zero_skip):
+    c = Case(B=1, Hkv=2, g=2, n=300, seed=77)
+    c.Q[0, 0, :5] = 0  # zero q channels exercise D1
+    c.q = torch.from_numpy(c.Q.view(np.int16)).view(c.B, c.Hkv * c.g, 128)
+    _compare_case(c, AlignConfig(margin, zero_skip), OAlignConfig(margin, zero_skip))
+
+
+def test_row_strategy_parity():
+    _compare_case(Case(B=1, Hkv=2, g=2, n=400, seed=9, lo=-1, hi=1), strategy="row")
+
+
+@pytest.mark.parametrize("tier", [8, 12, 16])
+def test_forced_tier_parity(tier):
+    _compare_case(Case(B=1, Hkv=2, g=1, n=300, seed=3), force=tier)
+
+
+def test_forced_t16_equals_reference_paths():
+    """SPEC.md:584 on the GPU: forced T16 == reference_scores/reference_output (bit-identical)."""
+    c = Case(B=2, Hkv=2, g=2, n=333, seed=21)
+    r = c.gpu(force_tier=16)
+    s_ref = AD.reference_scores(c.q, c.store)
+    assert torch.equal(r.scores, s_ref)
+    o_ref = AD.reference_output(r.probs, c.store)
+    assert torch.equal(r.o, o_ref)
+    # ... and agrees with a plain torch fp32 attention over the stored fp16 words
+    K = torch.from_numpy(c.K.view(np.int16)).view(torch.float16).float().cuda()
+    V = torch.from_numpy(c.V.view(np.int16)).view(torch.float16).float().cuda()
+    q = c.q.cuda().view(torch.float16).float().view(4, 2, 128)
+    s_t = torch.einsum("ugd,und->ugn", q, K) / np.sqrt(128)
+    p_t = torch.softmax(s_t.double(), -1).float()
+    o_t = torch.einsum("ugn,und->ugd", p_t, V)
+    assert close(r.o.view(4, 2, 128).cpu().numpy(), o_t.cpu().numpy())
+
+
+def test_baseline_truncated_parity():
+    c = Case(B=1, Hkv=2, g=1, n=300, seed=8)
+    r = c.gpu()
+    s_b, o_b = AD.baseline_truncated(c.q, c.store, r.probs, 13)
+    for u, b, hq, j in c.units():
+        s_ref, o_ref = OA.baseline_truncated(c.Q[u, j], c.K[u], r.probs[b, hq].cpu().numpy().astype(np.float64),
+                                             c.V[u], 13)
+        assert close(s_b[b, hq].cpu().numpy(), s_ref)
+        assert close(o_b[b, hq].cpu().numpy(), o_ref)
+
+
+def test_stepwise_api_matches_fused_step():
+    c = Case(B=1, Hkv=2, g=2, n=500, seed=31)
+    fused = c.gpu()
+    sv = AD.scores_aligned(c.q, c.store)
+    assert torch.equal(sv.s, fused.scores)
+    assert torch.equal(sv.k_tiers, fused.k_tiers)
+    p = AD.softmax(sv)
+    assert torch.equal(p.p, fused.probs)
+    est = AD.estimate_output(p, c.store)
+    assert torch.equal(est.o_est, fused.o_est)
+    o, vstats, vt = AD.output_aligned(p, c.store, est, export_v_tiers=True)
+    assert torch.equal(o, fused.o)
+    assert torch.equal(vt, fused.v_tiers)
+    with pytest.raises(ValueError, match="missing o_est"):
+        AD.output_aligned(p, c.store, None)
+
+
+def test_degenerate_q_raises():
+    c = Case(B=1, Hkv=1, g=1, n=20, seed=2)
+    with pytest.raises(DegenerateInputError, match="degenerate dot product"):
+        AD.decode_step(torch.zeros(1, 1, 128, dtype=torch.float16), c.store)
+
+
+def test_spec_examples_embedded():
+    """SPEC.md:321 (d=2 example embedded in d=128 with zero channels)."""
+    st = KVStore(1, 1, 128, 256)
+    k = np.zeros(128, np.uint16)
+    k[0], k[1] = ohb.encode(1.0), ohb.encode(7.0)
+    st.append_token(torch.from_numpy(k.view(np.int16)), torch.zeros(128, dtype=torch.int16))
+    q = np.zeros(128, np.uint16)
+    q[0] = ohb.encode(1.0)
+    sv = AD.scores_aligned(torch.from_numpy(q.view(np.int16)), st)
+    assert sv.s.item() == pytest.approx(1.0 / np.sqrt(128), rel=1e-7)  # d=128 scaling
+    assert sv.k_tiers[0, 0, 0].item() == 16 and (sv.k_tiers[0, 0, 1:] == 0).all()
+    assert sv.k_stats.bits_read == 16
+    # one-hot p -> o = V row exactly
+    st2 = KVStore(1, 1, 128, 256)
+    K = np.zeros((3, 128), np.uint16)
+    K[:, 0] = ohb.encode_array([1.0, 2000.0, 1.0])
+    V = ohb.encode_array(np.random.default_rng(0).standard_normal((3, 128)))
+    st2.append(torch.from_numpy(K.view(np.int16)), torch.from_numpy(V.view(np.int16)))
+    r = AD.decode_step(torch.from_numpy(q.view(np.int16)), st2)
+    assert np.array_equal(r.o[0, 0].cpu().numpy(), ohb.decode_array(V[1]).astype(np.float32))
+
+
+def test_error_histograms_match_oracle():
+    """Aligned-vs-full-fp16 error histograms (A-hist) within +-1 pp of the oracle's."""
+    c = Case(B=2, Hkv=2, g=1, n=1024, seed=7)
+    r = c.gpu()
+    rr = c.gpu(force_tier=16)
+    o_ref_gpu = AD.reference_output(r.probs, c.store)
+    rnd = ohb.float16_round
+    gq, oq, gs, os_ = [], [], [], []
+    for u, b, hq, j in c.units():
+        ref = c.oracle(u, j)
+        s_ref = OA.reference_scores(c.Q[u, j], c.K[u])
+        o_ref = OA.reference_output(ref.p, c.V[u])
+        gq.append(relative_error_histogram(rnd(r.scores[b, hq].cpu().numpy()), rnd(rr.scores[b, hq].cpu().numpy())))
+        oq.append(relative_error_histogram(rnd(ref.s), rnd(s_ref)))
+        gs.append(relative_error_histogram(rnd(r.o[b, hq].cpu().numpy()), rnd(o_ref_gpu[b, hq].cpu().numpy())))
+        os_.append(relative_error_histogram(rnd(ref.o), rnd(o_ref)))
+    assert np.abs(np.mean(gq, 0) - np.mean(oq, 0)).max() <= 0.01
+    assert np.abs(np.mean(gs, 0) - np.mean(os_, 0)).max() <= 0.01
+
+
+def test_determinism_and_ragged_lengths():
+    c = Case(B=2, Hkv=2, g=2, n=700, seed=13)
+    a = c.gpu()
+    b = c.gpu()
+    assert torch.equal(a.o, b.o) and torch.equal(a.counters, b.counters)
+    # ragged: shorten unit (b=0, h=1) on device -> its output equals the oracle on its first 300 tokens
+    c.store.lengths_dev[1] = 300
+    c.store._host_len[1] = 300
+    r = c.gpu()
+    from oracle.kv_store import KVStore as OStore
+    st = OStore(128)
+    st.append_rows(c.K[1][:300], c.V[1][:300])
+    st.colmax = c.store.colmax()[0, 1].cpu().numpy().astype(np.uint16)  # running max is not rewound
+    for j in range(2):
+        ref = OA.decode_head(c.Q[1, j], st)
+        assert np.array_equal(r.k_tiers[0, 2 + j].cpu().numpy(), ref.k_tiers)
+        assert close(r.o[0, 2 + j].cpu().numpy(), ref.o)
+    # the untouched units are unchanged
+    assert torch.equal(r.o[0, :2], a.o[0, :2]) and torch.equal(r.o[1], a.o[1])
