@@ -103,19 +103,21 @@ typedef struct {
   int32_t* sel_idx;     /* [U*g][AKV_MAX_KSEL] selected tokens, ascending */
   int32_t* head_meta;   /* [U*g][4] sel_count, min_target, any_unknown, n */
   float* head_metaf;    /* [U*g][4] M, L, pmax, thr */
-  float* o_partial;     /* [U*g][ceil(max_pages/AKV_PAGES_PER_CTA)][d] */
+  float* o_partial;     /* [U*g][max_pages][d] per-page partial outputs */
   float* o;             /* [U*g][d] attention output (out) */
   int64_t* counters;    /* [U*g][8] k8,k12,k16, v8,v12,v16, 0, 0 (elements) */
   int64_t* unit_bytes;  /* [U][4] physical plane bytes: K, V, 0, 0 */
   int64_t* status;      /* [U*g] */
   uint8_t* k_tiers;     /* [U*g][d] read-bit codes 0/8/12/16 (out) */
   uint8_t* v_tiers;     /* [U*g][cap][d] or NULL: per-element V codes (debug/parity) */
+  uint32_t* work;       /* [8] persistent-kernel work queues; zero before first use, self-resetting */
 } akv_step_t;
 
 int akv_version(void);
 
 /* Bytes of one contiguous workspace that akv_step_carve() splits into every
- * akv_step_t buffer except q, o and v_tiers. */
+ * akv_step_t buffer except q, o and v_tiers.  The workspace must be zeroed
+ * once before its first use (the work queues inside reset themselves). */
 int64_t akv_workspace_bytes(int32_t n_units, int32_t group, int32_t max_pages);
 int akv_step_carve(akv_step_t* step, void* workspace, int32_t n_units, int32_t group, int32_t max_pages);
 

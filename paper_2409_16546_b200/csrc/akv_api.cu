@@ -66,7 +66,7 @@ extern "C" int akv_version(void) { return AKV_VERSION; }
 static inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t max_pages) {
-  const int64_t H = (int64_t)U * G, cap = (int64_t)max_pages * P, nblk = (max_pages + 3) / 4;
+  const int64_t H = (int64_t)U * G, cap = (int64_t)max_pages * P;
   int64_t off = 0;
   auto take = [&](int64_t bytes) {
     uint8_t* p = ws ? ws + off : nullptr;
@@ -81,11 +81,12 @@ static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t 
   uint8_t* sel_idx = take(H * AKV_MAX_KSEL * 4);
   uint8_t* head_meta = take(H * 4 * 4);
   uint8_t* head_metaf = take(H * 4 * 4);
-  uint8_t* o_partial = take(H * nblk * D * 4);
+  uint8_t* o_partial = take(H * max_pages * D * 4);
   uint8_t* counters = take(H * 8 * 8);
   uint8_t* unit_bytes = take((int64_t)U * 4 * 8);
   uint8_t* status = take(H * 8);
   uint8_t* k_tiers = take(H * D);
+  uint8_t* work = take(8 * 4);
   if (st) {
     st->scores = reinterpret_cast<float*>(scores);
     st->probs = reinterpret_cast<float*>(scores);
@@ -101,6 +102,7 @@ static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t 
     st->unit_bytes = reinterpret_cast<int64_t*>(unit_bytes);
     st->status = reinterpret_cast<int64_t*>(status);
     st->k_tiers = k_tiers;
+    st->work = reinterpret_cast<uint32_t*>(work);
   }
   return off;
 }

@@ -2,25 +2,33 @@
 // rule2_targets for every (unit, q-head): one CTA each.
 //
 //  1. combine the per-page (max, sum exp) of the QK kernel -> M, L;
-//  2. p_t = exp(s_t - M) / L  (written to probs, may overwrite scores);
-//  3. approximate top-k: C = {t : p_t >= pmax * 2^-m}; if |C| > k_sel keep the
-//     k_sel largest by (p desc, t asc) via an exact 4-pass radix select on the
-//     fp32 bit patterns (p >= 0, so bit order = value order);
-//  4. o_est = sum_{t in sel, ascending t} p_t * V[t] read at T16;
-//  5. target_r = floor(log2|o_est_r|) - 10 (0 -> unknown), plus the minimum
+//  2. p_t = exp(s_t - M) / L (written to probs, may overwrite scores in
+//     place); tokens with p_t >= pmax * 2^-m are compacted into a shared
+//     candidate list (warp-aggregated atomics);
+//  3. |C| <= k_sel: the selection is C.  Otherwise the k_sel largest by
+//     (p desc, t asc): an exact 4-pass radix select on the fp32 bit patterns
+//     of the candidates (p >= 0, so bit order = value order), ties at the
+//     k-th value resolved by ascending t;
+//  4. the selection is sorted by t; o_est = sum_{t in sel} p_t * V[t] at T16
+//     (warps split the rows, fixed-order reduction);
+//  5. target_r = floor(log2|o_est_r|) - 10 (0 -> unknown) plus the minimum
 //     known target and an any-unknown flag for the PV superset rule (H6).
 #include "akv_common.cuh"
 
 namespace akv {
 
-constexpr int ST = 512;  // threads per select CTA
+constexpr int ST = 256;    // threads per select CTA
+constexpr int CAND = 2048; // shared candidate capacity (overflow -> global fallback scan)
 
 struct SelSmem {
   unsigned hist[256];
-  int wcnt[ST / 32][2];
-  int sel_idx[AKV_MAX_KSEL];
+  int cand_t[CAND];
+  float cand_p[CAND];
+  int sel[AKV_MAX_KSEL];
+  int sel_sorted[AKV_MAX_KSEL];
+  float part[ST / 32][D];
   float M, L;
-  int ncand, sel_count, need_eq;
+  int ncand, nsel, need_eq, neq;
   unsigned vstar;
   int tmin[4], tunk[4];
 };
@@ -56,118 +64,170 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
     if (lane == 0) {
       sm.M = m;
       sm.L = l;
+      sm.ncand = 0;
+      sm.nsel = 0;
+      sm.neq = 0;
     }
   }
-  if (tid < 256) sm.hist[tid] = 0;
   __syncthreads();
   const float M = sm.M, L = sm.L;
   const float pmax = 1.0f / L;  // = expf(0) / L, the argmax token's p
   const float thr = ldexpf(pmax, -cfg.m);
   const bool est = cfg.force_tier == 0 && cfg.trunc_bits == 0 && cfg.k_sel > 0;  // k_sel = 0: softmax only
+  const int k_sel = max(min(cfg.k_sel, AKV_MAX_KSEL), 1);
   const float* sc = st.scores + (size_t)h * cap;
   float* pr = st.probs + (size_t)h * cap;
+  uint32_t* bits = st.sel_bits + (size_t)h * (cap >> 5);
 
-  // 2. probabilities + candidate count
-  int ncand = 0;
-  for (int t = tid; t < n; t += ST) {
-    const float p = expf(sc[t] - M) / L;
-    pr[t] = p;
-    ncand += (p >= thr);
-  }
-  ncand = warp_sum_i(ncand);
-  if (lane == 0) sm.wcnt[warp][0] = ncand;
-  __syncthreads();
-  if (tid == 0) {
-    int c = 0;
-    for (int w = 0; w < ST / 32; ++w) c += sm.wcnt[w][0];
-    sm.ncand = c;
-    sm.vstar = 0;
-    sm.need_eq = 0;
-  }
-  __syncthreads();
-  const int k_sel = max(min(cfg.k_sel, AKV_MAX_KSEL), 1);
-  const bool capped = est && sm.ncand > k_sel;
-
-  // 3. radix select of the k_sel-th largest candidate key (only if capped)
-  if (capped) {
-    unsigned prefix = 0, mask = 0;
-    int k = k_sel;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int t = tid; t < n; t += ST) {
-        const float p = pr[t];
-        const unsigned key = __float_as_uint(p);
-        if (p >= thr && (key & mask) == prefix) atomicAdd(&sm.hist[(key >> shift) & 0xFF], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int cum = 0, dg = 255;
-        for (; dg > 0; --dg) {
-          if (cum + (int)sm.hist[dg] >= k) break;
-          cum += sm.hist[dg];
-        }
-        sm.need_eq = k - cum;  // keys with this digit still needed
-        sm.vstar = prefix | ((unsigned)dg << shift);
-      }
-      __syncthreads();
-      k = sm.need_eq;
-      prefix = sm.vstar;
-      mask |= 0xFFu << shift;
-      if (tid < 256) sm.hist[tid] = 0;
-      __syncthreads();
-    }
-  }
-  const unsigned vstar = sm.vstar;
-  const int need_eq = sm.need_eq;
-
-  // ordered pass: selection flags, bitmap words, ascending index list
-  int base_sel = 0, base_eq = 0;
-  const int words = (n + 31) >> 5;
+  // 2. probabilities, bitmap reset, candidate compaction
   for (int t0 = 0; t0 < n; t0 += ST) {
     const int t = t0 + tid;
-    bool cand = false, gt = false, eq = false;
-    if (t < n && est) {
-      const float p = pr[t];
-      cand = p >= thr;
-      const unsigned key = __float_as_uint(p);
-      gt = cand && key > vstar;
-      eq = cand && key == vstar;
+    bool cand = false;
+    float p = 0.f;
+    if (t < n) {
+      p = expf(sc[t] - M) / L;
+      pr[t] = p;
+      cand = est && p >= thr;
     }
-    const unsigned beq = __ballot_sync(0xFFFFFFFFu, eq);
-    if (lane == 0) sm.wcnt[warp][1] = __popc(beq);
-    __syncthreads();
-    int eq_before = base_eq;
-    for (int w = 0; w < warp; ++w) eq_before += sm.wcnt[w][1];
-    eq_before += __popc(beq & ((1u << lane) - 1u));
-    const bool sel = capped ? (gt || (eq && eq_before < need_eq)) : cand;
-    const unsigned bsel_ = __ballot_sync(0xFFFFFFFFu, sel);
-    if (lane == 0 && (t >> 5) < words) st.sel_bits[(size_t)h * (cap >> 5) + (t >> 5)] = bsel_;
-    if (lane == 0) sm.wcnt[warp][0] = __popc(bsel_);
-    __syncthreads();
-    int sel_before = base_sel;
-    for (int w = 0; w < warp; ++w) sel_before += sm.wcnt[w][0];
-    sel_before += __popc(bsel_ & ((1u << lane) - 1u));
-    if (sel && sel_before < AKV_MAX_KSEL) sm.sel_idx[sel_before] = t;
-    for (int w = 0; w < ST / 32; ++w) {
-      base_sel += sm.wcnt[w][0];
-      base_eq += sm.wcnt[w][1];
+    if (lane == 0 && t < n) bits[t >> 5] = 0u;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, cand);
+    if (b) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&sm.ncand, __popc(b));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      const int slot = base + __popc(b & ((1u << lane) - 1u));
+      if (cand && slot < CAND) {
+        sm.cand_t[slot] = t;
+        sm.cand_p[slot] = p;
+      }
     }
-    __syncthreads();
   }
-  const int cnt = min(base_sel, AKV_MAX_KSEL);
+  if (tid < 256) sm.hist[tid] = 0;
+  __syncthreads();
+  const int ncand = sm.ncand;
 
-  // 4-5. o_est over the selected rows (T16), targets
+  if (est) {
+    if (ncand <= k_sel) {
+      // 3a. every candidate is selected
+      for (int i = tid; i < ncand; i += ST) sm.sel[i] = sm.cand_t[i];
+      if (tid == 0) sm.nsel = ncand;
+    } else {
+      // 3b. radix select of the k_sel-th largest key among the candidates
+      const bool shared_list = ncand <= CAND;
+      unsigned prefix = 0, mask = 0;
+      int k = k_sel;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        if (shared_list) {
+          for (int i = tid; i < ncand; i += ST) {
+            const unsigned key = __float_as_uint(sm.cand_p[i]);
+            if ((key & mask) == prefix) atomicAdd(&sm.hist[(key >> shift) & 0xFF], 1u);
+          }
+        } else {
+          for (int t = tid; t < n; t += ST) {
+            const float p = pr[t];
+            const unsigned key = __float_as_uint(p);
+            if (p >= thr && (key & mask) == prefix) atomicAdd(&sm.hist[(key >> shift) & 0xFF], 1u);
+          }
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int cum = 0, dg = 255;
+          for (; dg > 0; --dg) {
+            if (cum + (int)sm.hist[dg] >= k) break;
+            cum += sm.hist[dg];
+          }
+          sm.need_eq = k - cum;
+          sm.vstar = prefix | ((unsigned)dg << shift);
+        }
+        __syncthreads();
+        k = sm.need_eq;
+        prefix = sm.vstar;
+        mask |= 0xFFu << shift;
+        sm.hist[tid] = 0;
+        __syncthreads();
+      }
+      const unsigned vstar = sm.vstar;
+      const int need_eq = sm.need_eq;
+      // keys > v* are all selected (fewer than k_sel); keys == v*: the need_eq smallest t
+      auto visit = [&](int t, float p) {
+        const unsigned key = __float_as_uint(p);
+        if (key > vstar) {
+          const int slot = atomicAdd(&sm.nsel, 1);
+          sm.sel[slot] = t;
+        } else if (key == vstar) {
+          const int slot = atomicAdd(&sm.neq, 1);
+          if (slot < CAND) sm.cand_t[slot] = t;  // reuse the candidate buffer (already consumed)
+        }
+      };
+      __syncthreads();
+      if (shared_list) {
+        // copy out first (visit overwrites cand_t)
+        int my_t[CAND / ST];
+        float my_p[CAND / ST];
+        int cnt = 0;
+        for (int i = tid; i < ncand; i += ST, ++cnt) {
+          my_t[cnt] = sm.cand_t[i];
+          my_p[cnt] = sm.cand_p[i];
+        }
+        __syncthreads();
+        for (int i = 0; i < cnt; ++i) visit(my_t[i], my_p[i]);
+      } else {
+        for (int t = tid; t < n; t += ST) {
+          const float p = pr[t];
+          if (p >= thr) visit(t, p);
+        }
+      }
+      __syncthreads();
+      // the need_eq smallest t among the ties (rank by counting; ties are rare)
+      const int neq = min(sm.neq, CAND);
+      const int base = sm.nsel;
+      for (int i = tid; i < neq; i += ST) {
+        const int t = sm.cand_t[i];
+        int rank = 0;
+        for (int j = 0; j < neq; ++j) rank += sm.cand_t[j] < t;
+        if (rank < need_eq) sm.sel[base + rank] = t;
+      }
+      __syncthreads();
+      if (tid == 0) sm.nsel = base + min(need_eq, neq);
+    }
+  }
+  __syncthreads();
+  const int cnt = est ? min(sm.nsel, AKV_MAX_KSEL) : 0;
+
+  // 4. sort the selection by t (rank by counting, <= 64 entries), bitmap, o_est
+  if (tid < cnt) {
+    const int t = sm.sel[tid];
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) rank += sm.sel[j] < t;
+    sm.sel_sorted[rank] = t;
+    atomicOr(bits + (t >> 5), 1u << (t & 31));
+  }
+  __syncthreads();
+  // rows split over warps (warp w: rows w, w+8, ...), lane = 4 channels; fixed-order reduction
+  {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = warp; i < cnt; i += ST / 32) {
+      const int t = sm.sel_sorted[i];
+      const uint8_t* vp = page_ptr(s.v_pool, s.page_table, s.max_pages, u, t / P);
+      const float p = pr[t];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t w = v_word_exact(vp, t % P, lane * 4 + e);
+        acc[e] = fmaf(p, __half2float(__ushort_as_half((unsigned short)w)), acc[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm.part[warp][lane * 4 + e] = acc[e];
+  }
+  __syncthreads();
   if (tid < D) {
     const int r = tid;
-    float acc = 0.f;
-    for (int i = 0; i < cnt; ++i) {
-      const int t = sm.sel_idx[i];
-      const uint8_t* vp = page_ptr(s.v_pool, s.page_table, s.max_pages, u, t / P);
-      const uint32_t w = v_word_exact(vp, t % P, r);
-      acc = fmaf(pr[t], __half2float(__ushort_as_half((unsigned short)w)), acc);
-    }
-    st.o_est[(size_t)h * D + r] = acc;
-    const bool known = acc != 0.f;
-    const int tg = known ? floor_log2f(acc) - 10 : AKV_TARGET_UNKNOWN;
+    float o = 0.f;
+#pragma unroll
+    for (int w = 0; w < ST / 32; ++w) o += sm.part[w][r];
+    st.o_est[(size_t)h * D + r] = o;
+    const bool known = o != 0.f;
+    const int tg = known ? floor_log2f(o) - 10 : AKV_TARGET_UNKNOWN;
     st.targets[(size_t)h * D + r] = tg;
     const int wmin = warp_min_i(known ? tg : INT_MAX);
     const int wunk = warp_sum_i(known ? 0 : 1);
@@ -175,7 +235,7 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
       sm.tmin[warp] = wmin;
       sm.tunk[warp] = wunk;
     }
-    if (r < cnt) st.sel_idx[(size_t)h * AKV_MAX_KSEL + r] = sm.sel_idx[r];
+    if (r < cnt) st.sel_idx[(size_t)h * AKV_MAX_KSEL + r] = sm.sel_sorted[r];
   }
   __syncthreads();
   if (tid == 0) {

@@ -59,8 +59,10 @@ def test_append_rejects_nonfinite_with_position():
     v2[0, 1, 77] = float("inf")
     with pytest.raises(ValueError, match=r"non-finite half word 0x7C00 in V at batch 0, kv-head 1, token 5, channel 77"):
         st.append_token(k2, v2)
-    assert st.lengths.tolist() == [[5, 5]]
-    assert st.lengths_dev.cpu().tolist() == [5, 5]
+    # per-unit semantics (each unit is one SPEC store): the finite unit commits, the offender does not
+    assert st.lengths.tolist() == [[6, 5]]
+    assert st.lengths_dev.cpu().tolist() == [6, 5]
+    st.rewind(5)
     kb = torch.randn(1, 2, 3, 128).half()
     kb[0, 0, 2, 9] = float("nan")
     with pytest.raises(ValueError, match=r"in K at batch 0, kv-head 0, token 7, channel 9"):
