@@ -31,7 +31,7 @@ namespace akv {
 enum : uint32_t { M_SKIP = 0, M_ELEM = 1, M_T8 = 8, M_T12 = 12, M_T16 = 16 };
 
 template <int G>
-struct PvWarp {
+struct alignas(16) PvWarp {
   float2 row[G][P];  // (p_t, bits(ep << 8 | mode)) per (head, row)
   int gthr[G][D];    // ELEMENT thresholds per (head, channel)
   uint8_t fl[P];     // union fetch flags: 2 = mid row, 4 = low row

@@ -61,7 +61,7 @@ __device__ __forceinline__ void fma8(const uint32_t w[4], uint32_t qpair, float 
 
 // Per-warp prologue state; lists are in "list order" (T8 class first).
 template <int G>
-struct QkWarp {
+struct alignas(16) QkWarp {
   uint32_t q[G][D / 2];  // q (fp16) per list position, pairs (2p, 2p+1); 0 for SKIP heads / pads
   uint2 hm[G][D];        // per-head (keep, fill) word masks per list position (used when G > 1)
   uint16_t ent[D];       // channel | class << 8 ; class 0 = pad
