@@ -111,6 +111,7 @@ typedef struct {
   uint8_t* k_tiers;     /* [U*g][d] read-bit codes 0/8/12/16 (out) */
   uint8_t* v_tiers;     /* [U*g][cap][d] or NULL: per-element V codes (debug/parity) */
   uint32_t* work;       /* [8] persistent-kernel work queues; zero before first use, self-resetting */
+  uint32_t* need_bits;  /* [U*g][2][cap/32] V rows needing the mid / low nibble row (superset rule) */
 } akv_step_t;
 
 int akv_version(void);

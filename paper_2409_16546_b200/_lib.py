@@ -42,7 +42,7 @@ class AkvCfg(ctypes.Structure):
 class AkvStep(ctypes.Structure):
     _fields_ = [(name, _c) for name in (
         "q", "scores", "probs", "page_stats", "o_est", "targets", "sel_bits", "sel_idx", "head_meta",
-        "head_metaf", "o_partial", "o", "counters", "unit_bytes", "status", "k_tiers", "v_tiers", "work")]
+        "head_metaf", "o_partial", "o", "counters", "unit_bytes", "status", "k_tiers", "v_tiers", "work", "need_bits")]
 
 
 _lock = threading.Lock()

@@ -280,6 +280,8 @@ class OutputEstimate:
     sel_idx: torch.Tensor
     v_stats: AccessCounter
     _ws: DecodeWorkspace = field(repr=False)
+    _k_sel: int = 32
+    _m: int = 5
 
     def selection(self, b: int, h: int) -> np.ndarray:
         return self.sel_idx[b, h, : int(self.sel_count[b, h])].cpu().numpy()
@@ -327,7 +329,7 @@ def estimate_output(p: Probabilities, store: KVStore, k_sel: int = 32, m: int = 
     meta = ws.head_meta().cpu()
     cnt = ws.counters().cpu().numpy().sum(0)
     return OutputEstimate(ws.o_est().clone().view(B, hq, -1), meta[:, 0].view(B, hq),
-                          ws.sel_idx().clone().view(B, hq, MAX_KSEL), AccessCounter(0, 0, int(cnt[5])), ws)
+                          ws.sel_idx().clone().view(B, hq, MAX_KSEL), AccessCounter(0, 0, int(cnt[5])), ws, k_sel, m)
 
 
 def output_aligned(p: Probabilities, store: KVStore, o_est: Optional[OutputEstimate] = None,
@@ -337,7 +339,9 @@ def output_aligned(p: Probabilities, store: KVStore, o_est: Optional[OutputEstim
         raise ValueError("missing o_est")
     ws = p._ws
     ws.set_v_tiers(export_v_tiers)
-    c = make_cfg(ws.group, cfg, 32, 5, strategy)
+    c = make_cfg(ws.group, cfg, o_est._k_sel, o_est._m, strategy)
+    # the PV fetch plan (need bits) depends on the strategy: re-run the (deterministic) select stage
+    _launch("akv_softmax_select", store, c, ws)
     ctr = ws.counters()
     before = ctr[:, 3:6].clone()
     _launch("akv_pv", store, c, ws)

@@ -87,6 +87,7 @@ static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t 
   uint8_t* status = take(H * 8);
   uint8_t* k_tiers = take(H * D);
   uint8_t* work = take(8 * 4);
+  uint8_t* need_bits = take(H * 2 * (cap / 32) * 4);
   if (st) {
     st->scores = reinterpret_cast<float*>(scores);
     st->probs = reinterpret_cast<float*>(scores);
@@ -103,6 +104,7 @@ static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t 
     st->status = reinterpret_cast<int64_t*>(status);
     st->k_tiers = k_tiers;
     st->work = reinterpret_cast<uint32_t*>(work);
+    st->need_bits = reinterpret_cast<uint32_t*>(need_bits);
   }
   return off;
 }

@@ -1,60 +1,65 @@
-// output_aligned for every (unit, q-head): persistent warps
-// pull (unit, page) items from an atomic queue; one item = one 256-token V
-// page; the page's partial output goes to o_partial[h][page] and the combine
-// kernel adds o_est and the partials in a fixed order (deterministic).
+// output_aligned for every (unit, q-head).
 //
-// Per item prologue (one lane per row) decides, for every row t and q-head j,
-// a mode:
-//   SKIP     t was selected by the estimate (D6: its T16 contribution is in
-//            o_est) or t >= n;
-//   T8       p_t == 0 (D5), or the RowMax superset bound shows every element of
-//            the row needs <= 2 kept bits (H6: e_v <= max(bexp(RowMax_t),1)-15,
-//            target_r >= min_r target_r);
-//   T8/T12/T16 forced tiers (D8), the row strategy (D7), baseline truncation;
-//   ELEMENT  per-element rule from the head byte's exponent (D4): keep mid iff
-//            max(bexp,1) + e(p_t) > 17 + target_r - margin, low iff > that + 4.
-// The union over the kv-head's q-heads decides which 64 B nibble rows are
-// fetched; per-element truncation is applied after the fetch, so the masks
-// are exactly the oracle's.
+// Warp-specialised persistent kernel, one CTA per SM:
 //
-// Main loop: 16 lanes per row x 8 channels per lane (LDG.64 head, LDG.32
-// mid/low), two rows per warp instruction, loads software-pipelined one
-// 16-row block ahead.  Blocks whose rows are all T8/SKIP take a branch-free
-// path (4 PRMT per 8 elements).  fp16 -> fp32 by HADD2.F32, p_t * V~ by the
-// packed FFMA2 into fp32 accumulators (>= 24-bit).
+//  producer warp   pulls (unit, page) items from an atomic queue, reads the
+//                  page's per-head "need mid / need low" row bitmaps written by
+//                  akv_softmax_select (RowMax superset rule; row
+//                  tiers for the row strategy, D7), and streams the page into
+//                  a shared ring with TMA bulk copies: the valid rows of the
+//                  head plane in one copy, only the runs of 64 B mid / low rows
+//                  that some q-head of the kv-head needs, and the per-row
+//                  metadata (p_t, selection bits, need bits, rule-2 targets);
+//  consumer warps  (two groups of four for G <= 2, one group for G >= 4) take
+//                  16 lanes per row x 8 channels per lane, two rows per warp
+//                  instruction.  Rows that no q-head needs beyond T8 take a
+//                  branch-free path (4 PRMT per 8 elements); otherwise each
+//                  head applies its own rule: selected rows are skipped (D6:
+//                  their T16 contribution is already in o_est), p_t = 0 rows
+//                  read T8 (D5), ELEMENT rows keep mid iff
+//                  max(bexp,1) + e(p_t) > 17 + target_r - margin and low iff
+//                  > that + 4 (D4), row-strategy rows use the row tier (D7).
+//                  Truncation is applied after the fetch, so the masks are the
+//                  oracle's bit for bit.  fp16 -> fp32 by HADD2.F32 and
+//                  p_t * V~ by the packed FFMA2 into fp32.
+// The page's partial output goes to o_partial[h][page]; akv_combine adds o_est
+// and the partials in a fixed order (deterministic).
 #include <algorithm>
 
 #include "akv_common.cuh"
 
 namespace akv {
 
-enum : uint32_t { M_SKIP = 0, M_ELEM = 1, M_T8 = 8, M_T12 = 12, M_T16 = 16 };
-
 template <int G>
-struct alignas(16) PvWarp {
-  float2 row[G][P];  // (p_t, bits(ep << 8 | mode)) per (head, row)
-  int gthr[G][D];    // ELEMENT thresholds per (head, channel)
-  uint8_t fl[P];     // union fetch flags: 2 = mid row, 4 = low row
-  uint32_t blk_slow;
-};
-
-struct VBatch {
-  uint2 h[8];
-  uint32_t m[8], l[8];
+struct PvShape {
+  static constexpr int NG = G >= 4 ? 1 : 2;       // consumer groups (pages in flight)
+  static constexpr int NS = G >= 4 ? 2 : 3;       // ring stages
+  static constexpr int THREADS = 32 * (1 + 4 * NG);
 };
 
 template <int G>
-__device__ __forceinline__ void v_load(VBatch& X, const PvWarp<G>& ws, int blk, int half, const uint8_t* hb,
-                                       const uint8_t* mb, uint64_t pol) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = blk * 16 + 2 * i + half;
-    const uint32_t f = ws.fl[r];
-    X.h[i] = ld_stream_u64(hb + (blk * 16 + 2 * i) * D, pol);
-    if (f & 2) X.m[i] = ld_stream_u32(mb + (blk * 16 + 2 * i) * (D / 2), pol);
-    if (f & 4) X.l[i] = ld_stream_u32(mb + (blk * 16 + 2 * i) * (D / 2) + (LOW - MID), pol);
-  }
-}
+struct alignas(16) PvAux {   // TMA-copied per-row / per-head metadata of one page
+  float probs[G][P];
+  int32_t targets[G][D];
+  uint32_t sel[G][8];
+  uint32_t need[G][2][8];
+};
+
+struct alignas(16) PvMeta {
+  int item, u, pg, n;
+  uint32_t un_mid[8], un_low[8];  // union over q-heads of the need bitmaps (rows of this page)
+};
+
+template <int G>
+struct alignas(128) PvSmem {
+  uint8_t data[PvShape<G>::NS][PAGE];
+  PvAux<G> aux[PvShape<G>::NS];
+  PvMeta meta[PvShape<G>::NS];
+  float red[PvShape<G>::NG][4][G][D];
+  uint64_t full[PvShape<G>::NS], empty[PvShape<G>::NS];
+};
+
+__device__ __forceinline__ bool bit8(const uint32_t* w, int r) { return (w[r >> 5] >> (r & 31)) & 1u; }
 
 __device__ __forceinline__ void t8_words(uint2 h, uint32_t w[4]) {
   const uint32_t c80 = 0x80808080u;
@@ -64,90 +69,133 @@ __device__ __forceinline__ void t8_words(uint2 h, uint32_t w[4]) {
   w[3] = prmt(h.y, c80, 0x3424);
 }
 
-template <int G, bool TRUNC, bool EXPORT>
-__device__ __forceinline__ void v_compute(const VBatch& X, const PvWarp<G>& ws, int blk, int half, int cl,
-                                          float2 acc[G][4], int cnt[G][3], uint32_t tkm, uint32_t tf,
-                                          uint8_t* vt_row0, size_t vt_head_stride, int rows_valid) {
-  const bool slow = (ws.blk_slow >> blk) & 1u;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = blk * 16 + 2 * i + half;
-    if (!slow) {
-      // every row of the block is T8 or SKIP (p = 0) for every head
-      uint32_t w[4];
-      t8_words(X.h[i], w);
-      float2 f[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) f[k] = half2_bits_to_float2(w[k]);
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const float p = ws.row[j][r].x;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(f[k], p, acc[j][k]);
-        if (EXPORT && vt_row0 && r < rows_valid) {
-          const uint32_t mode = __float_as_uint(ws.row[j][r].y) & 0xFFu;
-          const uint32_t c = mode == M_SKIP ? 0x10101010u : 0x08080808u;
-          *reinterpret_cast<uint2*>(vt_row0 + j * vt_head_stride + (size_t)r * D + cl * 8) = make_uint2(c, c);
-        }
-      }
-      continue;
+// ----------------------------------------------------------------------------
+// producer
+// ----------------------------------------------------------------------------
+struct PvPrefetch {
+  int item, u, pg, n;
+  uint32_t um, ul;  // lane w < 8: union need words w of this page
+};
+
+template <int G>
+__device__ __forceinline__ void pv_grab(PvPrefetch& f, const akv_store_t& s, const akv_cfg_t& cfg,
+                                        const akv_step_t& st, int npg_max, unsigned total, int cap, bool uniform) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned item = 0;
+    if (lane == 0) item = atomicAdd(st.work + 2, 1u);
+    item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    if (item >= total) {
+      f.item = -1;
+      return;
     }
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float2 rw = ws.row[j][r];
-      const uint32_t em = __float_as_uint(rw.y);
-      const uint32_t mode = em & 0xFFu;
-      uint32_t w[4];
-      uint32_t code_lo = 0, code_hi = 0;
-      if (mode != M_ELEM) {
-        const TierMask tm = tier_mask(mode == M_SKIP ? 8 : (int)mode);
-        assemble8(X.h[i].x, X.h[i].y, bsel(tm.mk, X.m[i], 0x88888888u), bsel(tm.lk, X.l[i], tm.lf), w);
-        if (EXPORT) code_lo = code_hi = (mode == M_SKIP ? 16u : mode) * 0x01010101u;
+    const int u = item / npg_max, pg = item % npg_max;
+    const int n = s.lengths[u];
+    if (pg * P >= n) continue;
+    f.item = (int)item;
+    f.u = u;
+    f.pg = pg;
+    f.n = n;
+    f.um = f.ul = 0u;
+    if (lane < 8) {
+      if (uniform) {
+        f.um = cfg.force_tier >= 12 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
+        f.ul = cfg.force_tier >= 16 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
       } else {
-        assemble8(X.h[i].x, X.h[i].y, X.m[i], X.l[i], w);
-        const int ep = (int)em >> 8;
-        const int4 g0 = *reinterpret_cast<const int4*>(&ws.gthr[j][cl * 8]);
-        const int4 g1 = *reinterpret_cast<const int4*>(&ws.gthr[j][cl * 8 + 4]);
-        const int gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t hbyte = ((e < 4 ? X.h[i].x : X.h[i].y) >> (8 * (e & 3))) & 0xFFu;
-          const int E = max((int)((hbyte >> 2) & 31u), 1) + ep;
-          const bool km = E > gg[e], kl = E > gg[e] + 4;
-          const int sh = 16 * (e & 1);
-          uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
-          w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
-          w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
-          cnt[j][kl ? 2 : (km ? 1 : 0)] += 1;
-          if (EXPORT) {
-            const uint32_t cd = kl ? 16u : (km ? 12u : 8u);
-            if (e < 4) code_lo |= cd << (8 * e);
-            else code_hi |= cd << (8 * (e - 4));
-          }
+        for (int j = 0; j < G; ++j) {
+          const uint32_t* nb = st.need_bits + ((size_t)u * G + j) * 2 * (cap >> 5) + pg * 8 + lane;
+          f.um |= nb[0];
+          f.ul |= nb[cap >> 5];
         }
       }
-      if (TRUNC) {
+      // rows beyond n hold stale bits
+      const int lo = lane * 32, valid = min(max(n - pg * P - lo, 0), 32);
+      const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+      f.um &= vm;
+      f.ul &= vm;
+    }
+    return;
+  }
+}
+
+template <int G>
+__device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const akv_store_t& s,
+                           const akv_step_t& st, int cap) {
+  const int lane = threadIdx.x & 31;
+  PvMeta& mt = sm.meta[stage];
+  uint32_t um[8], ul[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
-      }
+  for (int w = 0; w < 8; ++w) {
+    um[w] = __shfl_sync(0xFFFFFFFFu, f.um, w);
+    ul[w] = __shfl_sync(0xFFFFFFFFu, f.ul, w);
+  }
+  int nm = 0, nl = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(half2_bits_to_float2(w[k]), rw.x, acc[j][k]);
-      if (EXPORT && vt_row0 && r < rows_valid)
-        *reinterpret_cast<uint2*>(vt_row0 + j * vt_head_stride + (size_t)r * D + cl * 8) = make_uint2(code_lo, code_hi);
+  for (int w = 0; w < 8; ++w) {
+    nm += __popc(um[w]);
+    nl += __popc(ul[w]);
+  }
+  const int rows = min(f.n - f.pg * P, P);
+  if (lane == 0) {
+    mt.item = f.item;
+    mt.u = f.u;
+    mt.pg = f.pg;
+    mt.n = f.n;
+  }
+  if (lane < 8) {
+    mt.un_mid[lane] = um[lane];
+    mt.un_low[lane] = ul[lane];
+  }
+  const uint8_t* src = page_ptr(s.v_pool, s.page_table, s.max_pages, f.u, f.pg);
+  uint8_t* dst = sm.data[stage];
+  PvAux<G>& ax = sm.aux[stage];
+  const uint32_t vbytes = (uint32_t)rows * D + (uint32_t)(nm + nl) * (D / 2);
+  const uint32_t abytes = (uint32_t)sizeof(PvAux<G>);
+  __syncwarp();
+  if (lane == 0) {
+    mbar_arrive_expect_tx(&sm.full[stage], vbytes + abytes);
+    atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)f.u * 4 + 1), (unsigned long long)vbytes);
+  }
+  __syncwarp();
+  if (lane == 31) bulk_g2s(dst, src, (uint32_t)rows * D, &sm.full[stage]);
+  if (lane < G) {
+    const size_t h = (size_t)f.u * G + lane;
+    bulk_g2s(ax.probs[lane], st.probs + h * cap + (size_t)f.pg * P, P * 4, &sm.full[stage]);
+    bulk_g2s(ax.targets[lane], st.targets + h * D, D * 4, &sm.full[stage]);
+    bulk_g2s(ax.sel[lane], st.sel_bits + h * (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
+    bulk_g2s(ax.need[lane][0], st.need_bits + h * 2 * (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
+    bulk_g2s(ax.need[lane][1], st.need_bits + h * 2 * (cap >> 5) + (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
+  }
+  // runs of rows needing the mid / low nibble row; lane l scans rows [8l, 8l+8)
+#pragma unroll
+  for (int pl = 0; pl < 2; ++pl) {
+    const uint32_t* mk = pl == 0 ? um : ul;
+    const int off = pl == 0 ? MID : LOW;
+    for (int r = lane * 8; r < lane * 8 + 8; ++r) {
+      if (!bit8(mk, r) || (r > 0 && bit8(mk, r - 1))) continue;
+      int e = r + 1;
+      while (e < P && bit8(mk, e)) ++e;
+      bulk_g2s(dst + off + r * (D / 2), src + off + r * (D / 2), (uint32_t)(e - r) * (D / 2), &sm.full[stage]);
     }
   }
 }
 
+// ----------------------------------------------------------------------------
+// consumer
+// ----------------------------------------------------------------------------
 template <int G, bool TRUNC, bool EXPORT>
-__global__ void __launch_bounds__(128) pv_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, int npg_max) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  PvWarp<G>& ws = reinterpret_cast<PvWarp<G>*>(smem_raw)[warp];
-  const uint64_t pol = evict_first_policy();
-  const unsigned total = (unsigned)s.n_units * npg_max;
-  const bool aligned = cfg.force_tier == 0 && !TRUNC;
-  const uint32_t uniform = TRUNC ? 16u : (uint32_t)cfg.force_tier;
+__device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, int w4, const akv_cfg_t& cfg,
+                                           const akv_step_t& st, int cap) {
+  const int lane = threadIdx.x & 31;
   const int half = lane >> 4, cl = lane & 15;
+  const PvMeta& mt = sm.meta[stage];
+  const PvAux<G>& ax = sm.aux[stage];
+  const uint8_t* pgd = sm.data[stage];
+  const int u = mt.u, pg = mt.pg, n = mt.n;
+  const int rows = min(n - pg * P, P);
+  const bool aligned = cfg.force_tier == 0 && !TRUNC;
+  const int uni = TRUNC ? 16 : cfg.force_tier;
   uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
   if (TRUNC) {
     const int kb = cfg.trunc_bits - 6;
@@ -156,151 +204,210 @@ __global__ void __launch_bounds__(128) pv_kernel(akv_store_t s, akv_cfg_t cfg, a
     tkm = km | (km << 16);
     tf = fill | (fill << 16);
   }
-
-  for (;;) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(st.work + 2, 1u);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= total) break;
-    const int u = item / npg_max, pg = item % npg_max;
-    const int n = s.lengths[u];
-    if (pg * P >= n) continue;
-    const int rows_valid = min(n - pg * P, P);
-
-    // ---------------- prologue: modes per (head, row) ----------------
-    int cnt[G][3];
-    int min_t[G], unk[G];
+  float2 acc[G][4];
+  int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8"
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      cnt[j][0] = cnt[j][1] = cnt[j][2] = 0;
-      const int32_t* hm = st.head_meta + ((size_t)u * G + j) * 4;
-      min_t[j] = hm[1];
-      unk[j] = hm[2];
+  for (int j = 0; j < G; ++j) {
+    adj[j][0] = adj[j][1] = adj[j][2] = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int tg = st.targets[((size_t)u * G + j) * D + lane + 32 * k];
-        ws.gthr[j][lane + 32 * k] = tg == AKV_TARGET_UNKNOWN ? -(1 << 20) : 17 + tg - cfg.margin_bits;
-      }
-    }
-    long long vbytes = 0;
-    uint32_t blk_slow = 0;
-#pragma unroll 1
-    for (int k = 0; k < 8; ++k) {
-      const int r = lane + 32 * k;
-      const int t = pg * P + r;
-      uint32_t fl = 0;
-      bool nont8 = false;
-      const uint32_t rm = t < n ? s.rowmax[(size_t)u * s.max_pages * P + t] : 0u;
-      const int e_rm = max(bexp16(rm), 1) - 15;  // D4 bound on every element's e_v
+    for (int k = 0; k < 4; ++k) acc[j][k] = make_float2(0.f, 0.f);
+  }
+  uint8_t* vt = (EXPORT && st.v_tiers) ? st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P) * D + cl * 8 : nullptr;
+
+  const int r0 = w4 * 64;
+#pragma unroll 2
+  for (int i = 0; i < 32; ++i) {
+    const int r = r0 + 2 * i + half;
+    if (r >= rows) continue;
+    const uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
+    const bool nm = bit8(mt.un_mid, r);
+    if (aligned && !nm) {
+      // no q-head needs more than the head byte on this row: T8 (or skipped)
+      uint32_t w[4];
+      t8_words(h, w);
+      float2 f[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) f[k] = half2_bits_to_float2(w[k]);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const size_t h = (size_t)u * G + j;
-        uint32_t mode = M_SKIP;
-        float p = 0.f;
-        int ep = -30000;
-        if (t < n) {
-          p = st.probs[h * cap + t];
-          if (p > 0.f) ep = floor_log2f(p);
-          if (!aligned) {
-            mode = uniform;
-          } else if ((st.sel_bits[h * (cap >> 5) + (t >> 5)] >> (t & 31)) & 1u) {
-            mode = M_SKIP;
-            p = 0.f;
-          } else if (cfg.strategy == 1) {  // row strategy (D7)
-            if (unk[j]) mode = M_T16;
-            else if (p == 0.f || rm == 0) mode = M_T8;
-            else {
-              const int tr = min(max(ep + magexp16(rm) + 1 - min_t[j] - 1 + cfg.margin_bits, 0), 10);
-              mode = tr <= 2 ? M_T8 : (tr <= 6 ? M_T12 : M_T16);
-            }
-          } else if (p == 0.f) {
-            mode = M_T8;  // D5
-          } else if (unk[j]) {
-            mode = M_ELEM;
-            fl |= 6;
-          } else {
-            const int bound = ep + e_rm + 1 - min_t[j] - 1 + cfg.margin_bits;  // superset t_req (H6)
-            if (bound > 2) {
-              mode = M_ELEM;
-              fl |= bound > 6 ? 6 : 2;
-            } else {
-              mode = M_T8;
-            }
-          }
+        const bool sel = bit8(ax.sel[j], r);
+        const float p = sel ? 0.f : ax.probs[j][r];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(f[k], p, acc[j][k]);
+        if (EXPORT && vt) {
+          const uint32_t c = sel ? 0x10101010u : 0x08080808u;
+          *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(c, c);
         }
-        if (mode == M_T12) fl |= 2;
-        if (mode == M_T16) fl |= 6;
-        if (mode == M_T8) cnt[j][0] += D;
-        if (mode == M_T12) cnt[j][1] += D;
-        if (mode == M_T16) cnt[j][2] += D;
-        nont8 |= mode != M_SKIP && mode != M_T8;
-        ws.row[j][r] = make_float2(p, __uint_as_float(((uint32_t)ep << 8) | mode));
       }
-      ws.fl[r] = (uint8_t)fl;
-      if (t < n) vbytes += D + ((fl & 2) ? D / 2 : 0) + ((fl & 4) ? D / 2 : 0);
-      const uint32_t bs = __ballot_sync(0xFFFFFFFFu, nont8);
-      blk_slow |= (((bs & 0xFFFFu) ? 1u : 0u) << (2 * k)) | (((bs >> 16) ? 1u : 0u) << (2 * k + 1));
+      continue;
     }
-    if (lane == 0) ws.blk_slow = blk_slow;
-    __syncwarp();
-
-    // ---------------- main loop ----------------
-    const uint8_t* base = page_ptr(s.v_pool, s.page_table, s.max_pages, u, pg);
-    const uint8_t* hb = base + half * D + cl * 8;
-    const uint8_t* mb = base + MID + half * (D / 2) + cl * 4;
-    const int nblk = (rows_valid + 15) >> 4;
-    float2 acc[G][4];
-#pragma unroll
-    for (int j = 0; j < G; ++j)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[j][k] = make_float2(0.f, 0.f);
-    uint8_t* vt0 = nullptr;
-    size_t vstride = 0;
-    if (EXPORT && st.v_tiers) {
-      vt0 = st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P) * D;
-      vstride = (size_t)cap * D;
-    }
-    VBatch A, B;
-    v_load<G>(A, ws, 0, half, hb, mb, pol);
-    for (int b = 0; b < nblk; b += 2) {
-      if (b + 1 < nblk) v_load<G>(B, ws, b + 1, half, hb, mb, pol);
-      v_compute<G, TRUNC, EXPORT>(A, ws, b, half, cl, acc, cnt, tkm, tf, vt0, vstride, rows_valid);
-      if (b + 1 >= nblk) break;
-      if (b + 2 < nblk) v_load<G>(A, ws, b + 2, half, hb, mb, pol);
-      v_compute<G, TRUNC, EXPORT>(B, ws, b + 1, half, cl, acc, cnt, tkm, tf, vt0, vstride, rows_valid);
-    }
-
-    // ---------------- epilogue: partial o of this page, counters ----------------
+    const uint32_t mv = nm ? *reinterpret_cast<const uint32_t*>(pgd + MID + r * (D / 2) + cl * 4) : 0u;
+    const bool nl = bit8(mt.un_low, r);
+    const uint32_t lv = nl ? *reinterpret_cast<const uint32_t*>(pgd + LOW + r * (D / 2) + cl * 4) : 0u;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const size_t h = (size_t)u * G + j;
+      const float p = ax.probs[j][r];
+      int mode;  // 0 skip, 1 element, 8/12/16 uniform tier
+      if (!aligned) mode = uni;
+      else if (bit8(ax.sel[j], r)) mode = 0;
+      else if (!bit8(ax.need[j][0], r)) mode = 8;  // includes p == 0 (D5)
+      else if (cfg.strategy == 1) mode = bit8(ax.need[j][1], r) ? 16 : 12;
+      else mode = 1;
+      uint32_t w[4];
+      uint32_t clo = 0, chi = 0;
+      if (mode == 0) {
+        if (EXPORT && vt) *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(0x10101010u, 0x10101010u);
+        continue;
+      } else if (mode != 1) {
+        const TierMask tm = tier_mask(mode);
+        assemble8(h.x, h.y, bsel(tm.mk, mv, 0x88888888u), bsel(tm.lk, lv, tm.lf), w);
+        if (aligned && mode != 8) {
+          adj[j][0] -= 8;
+          adj[j][mode == 12 ? 1 : 2] += 8;
+        }
+        if (EXPORT) clo = chi = (uint32_t)mode * 0x01010101u;
+      } else {
+        assemble8(h.x, h.y, mv, lv, w);
+        const int ep = p > 0.f ? floor_log2f(p) : -30000;
+        const int4 t0 = *reinterpret_cast<const int4*>(&ax.targets[j][cl * 8]);
+        const int4 t1 = *reinterpret_cast<const int4*>(&ax.targets[j][cl * 8 + 4]);
+        const int tg[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[j][k].x += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].x, 16);
-        acc[j][k].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].y, 16);
+        for (int e = 0; e < 8; ++e) {
+          const int g = tg[e] == AKV_TARGET_UNKNOWN ? -(1 << 20) : 17 + tg[e] - cfg.margin_bits;
+          const uint32_t hbyte = ((e < 4 ? h.x : h.y) >> (8 * (e & 3))) & 0xFFu;
+          const int E = max((int)((hbyte >> 2) & 31u), 1) + ep;
+          const bool km = E > g, kl = E > g + 4;
+          const int sh = 16 * (e & 1);
+          uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
+          w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
+          w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
+          if (km) {
+            adj[j][0] -= 1;
+            adj[j][kl ? 2 : 1] += 1;
+          }
+          if (EXPORT) {
+            const uint32_t cd = kl ? 16u : (km ? 12u : 8u);
+            if (e < 4) clo |= cd << (8 * e);
+            else chi |= cd << (8 * (e - 4));
+          }
+        }
       }
-      if (half == 0) {
-        float4* dst = reinterpret_cast<float4*>(st.o_partial + (h * s.max_pages + pg) * D + cl * 8);
-        dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
-        dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
+      if (TRUNC) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
       }
-      const int a = warp_sum_i(cnt[j][0]), bq = warp_sum_i(cnt[j][1]), c = warp_sum_i(cnt[j][2]);
-      if (lane == 0) {
-        unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + h * 8 + 3);
-        if (a) atomicAdd(ct + 0, (unsigned long long)a);
-        if (bq) atomicAdd(ct + 1, (unsigned long long)bq);
-        if (c) atomicAdd(ct + 2, (unsigned long long)c);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(half2_bits_to_float2(w[k]), p, acc[j][k]);
+      if (EXPORT && vt) *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(clo, chi);
+    }
+  }
+  // base counts: every valid unselected row at T8 (aligned) or at the uniform tier
+  if (w4 == 0 && lane < G) {
+    const int j = lane;
+    int nsel = 0;
+    if (aligned) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int lo = w * 32, valid = min(max(rows - lo, 0), 32);
+        const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+        nsel += __popc(ax.sel[j][w] & vm);
       }
     }
-    vbytes = warp_sum_ll(vbytes);
-    if (lane == 0)
-      atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)u * 4 + 1), (unsigned long long)vbytes);
-    __syncwarp();
+    const int slot = aligned ? 0 : (uni == 8 ? 0 : (uni == 12 ? 1 : 2));
+    adj[j][slot] += (rows - nsel) * D;
   }
-  if (lane == 0) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
+
+  // partial o: half-warps -> warps (shared) -> page
+  float* red = &sm.red[grp][w4][0][0];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc[j][k].x += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].x, 16);
+      acc[j][k].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].y, 16);
+    }
+    if (half == 0) {
+      float4* dst = reinterpret_cast<float4*>(red + j * D + cl * 8);
+      dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+      dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
+    }
+    const int a = warp_sum_i(adj[j][0]), b = warp_sum_i(adj[j][1]), c = warp_sum_i(adj[j][2]);
+    if (lane == 0) {
+      unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + ((size_t)u * G + j) * 8 + 3);
+      if (a) atomicAdd(ct + 0, (unsigned long long)(long long)a);
+      if (b) atomicAdd(ct + 1, (unsigned long long)(long long)b);
+      if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
+    }
+  }
+  named_bar(1 + grp, 128);
+  for (int j = w4; j < G; j += 4) {
+    const float4 a = *reinterpret_cast<const float4*>(&sm.red[grp][0][j][lane * 4]);
+    const float4 b = *reinterpret_cast<const float4*>(&sm.red[grp][1][j][lane * 4]);
+    const float4 c = *reinterpret_cast<const float4*>(&sm.red[grp][2][j][lane * 4]);
+    const float4 d = *reinterpret_cast<const float4*>(&sm.red[grp][3][j][lane * 4]);
+    const float4 o = make_float4((a.x + b.x) + (c.x + d.x), (a.y + b.y) + (c.y + d.y), (a.z + b.z) + (c.z + d.z),
+                                 (a.w + b.w) + (c.w + d.w));
+    *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + lane * 4) = o;
+  }
+  named_bar(1 + grp, 128);
+}
+
+template <int G, bool TRUNC, bool EXPORT>
+__global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st,
+                                                                    int cap, int npg_max) {
+  constexpr int NS = PvShape<G>::NS, NG = PvShape<G>::NG;
+  extern __shared__ __align__(128) uint8_t pv_smem_raw[];
+  PvSmem<G>& sm = *reinterpret_cast<PvSmem<G>*>(pv_smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 4);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const unsigned total = (unsigned)s.n_units * npg_max;
+  const bool uniform = cfg.force_tier != 0 || TRUNC;
+
+  if (warp == 0) {
+    PvPrefetch cur, nxt;
+    pv_grab<G>(nxt, s, cfg, st, npg_max, total, cap, uniform);
+    int k = 0;
+    for (;; ++k) {
+      cur = nxt;
+      if (cur.item < 0) break;
+      pv_grab<G>(nxt, s, cfg, st, npg_max, total, cap, uniform);
+      const int stage = k % NS;
+      mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
+      pv_produce<G>(sm, cur, stage, s, st, cap);
+    }
+    for (int t = 0; t < NG; ++t, ++k) {
+      const int stage = k % NS;
+      mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
+      if (lane == 0) {
+        sm.meta[stage].item = -1;
+        mbar_arrive(&sm.full[stage]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
+    for (int k = grp;; k += NG) {
+      const int stage = k % NS;
+      mbar_wait(&sm.full[stage], (k / NS) & 1);
+      if (sm.meta[stage].item < 0) break;
+      pv_consume<G, TRUNC, EXPORT>(sm, stage, grp, w4, cfg, st, cap);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
     const unsigned done = atomicAdd(st.work + 3, 1u);
-    if (done == gridDim.x * 4 - 1) {
+    if (done == gridDim.x - 1) {
       st.work[2] = 0;
       st.work[3] = 0;
       __threadfence();
@@ -325,29 +432,22 @@ __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t c
   st.o[(size_t)h * D + threadIdx.x] = acc;
 }
 
-template <typename K>
-static int resident_blocks_pv(K kernel, size_t smem) {
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, smem);
-  return std::max(1, sms * std::max(per, 1));
-}
-
 template <int G, bool TRUNC, bool EXPORT>
 static void launch_pv_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
-  const size_t smem = 4 * sizeof(PvWarp<G>);
-  static int resident = 0;
-  if (!resident) {
+  static int sms = 0;
+  const size_t smem = sizeof(PvSmem<G>);
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(pv_kernel<G, TRUNC, EXPORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    resident = resident_blocks_pv(pv_kernel<G, TRUNC, EXPORT>, smem);
   }
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, (items + 3) / 4);
-  pv_kernel<G, TRUNC, EXPORT><<<std::max(grid, 1), 128, smem, stream>>>(s, cfg, st, cap, npg);
+  const int grid = (int)std::min<long long>(sms, std::max<long long>(items / 2, 1));
+  pv_kernel<G, TRUNC, EXPORT><<<grid, PvShape<G>::THREADS, smem, stream>>>(s, cfg, st, cap, npg);
 }
 
 template <int G>

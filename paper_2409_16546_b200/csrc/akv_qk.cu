@@ -1,29 +1,37 @@
 // scores_aligned for every (unit, q-head) of a batch.
 //
-// Persistent warps pull (unit, page) items from an atomic queue (no wave
-// tail; deterministic because each page's result does not depend on which
-// warp computes it).  Per item a warp:
+// Warp-specialised persistent kernel, one CTA per SM:
 //
-//  1. evaluates Rule 1 for its unit (rule1_target SPEC.md:157-165,
-//     required_mantissa_bits :139-147, tier_for_bits :148-156,
-//     k_channel_tiers :175-183) for every q-head
-//     of the kv-head, and builds a channel list ordered by union class:
-//     T8 channels first (head plane only), then T12/T16 channels; SKIP
-//     channels are dropped (0 bits read);
-//  2. streams the page: lane = 8 consecutive tokens; per listed channel one
-//     LDG.64 of the 256 B head-plane row and, only for T12/T16 channels, one
-//     LDG.32 of the 128 B mid row (+ low row for T16).  Loads are
-//     software-pipelined one 8-channel batch ahead (ping-pong registers);
-//  3. rebuilds fp16 words with PRMT/LOP3 (midpoint fill for absent nibbles,
-//     HB:160-179) and accumulates q_c * K~ with the mixed-precision FHFMA
-//     (exact fp16 x fp16 products, fp32 sums, D9);
-//  4. scales by 1/sqrt(d) after accumulation and writes the
-//     page's scores and (max, sum exp) for the split softmax.
+//  producer warp   pulls (unit, page) items from an atomic queue (no wave
+//                  tail), evaluates Rule 1 for the unit's q-heads
+//                  (rule1_target SPEC.md:157-165, required_mantissa_bits
+//                  :139-147, tier_for_bits :148-156, k_channel_tiers :175-183,
+//                  SURVEY App. A A-K/D1/D2/D8), publishes the channel list and
+//                  tier codes, and streams the page into a 3-stage shared
+//                  ring with TMA bulk copies (cp.async.bulk + mbarrier
+//                  complete_tx): the whole 32 KB head plane in one copy, and
+//                  only the runs of 128 B mid / low channel rows whose union
+//                  tier needs them (SKIP / T8 channels read 8 bits or nothing);
+//  2 x 4 consumer  warps (two pages in flight) rebuild the fp16 words from
+//                  shared memory with PRMT/LOP3 (midpoint fill for absent
+//                  nibbles, HB:160-179) and accumulate q_c * K~ with the
+//                  mixed-precision FHFMA (exact fp16 x fp16 products, fp32
+//                  sums, D9); the 1/sqrt(d) scale is applied
+//                  after accumulation; each page also yields its
+//                  (max, sum exp) for the split softmax.
+//
+// Work split inside a consumer group: G = 1, 2 split the channel list (4 or 2
+// ways) and reduce partial sums through shared memory; G >= 4 give every warp
+// G/4 heads over all channels (no reduction).  Results do not depend on which
+// CTA / group processes a page, so the kernel is deterministic.
 #include <algorithm>
 
 #include "akv_common.cuh"
 
 namespace akv {
+
+constexpr int QK_NS = 3;                         // ring stages
+constexpr int QK_THREADS = 32 * 9;               // 1 producer + 8 consumer warps
 
 template <int E, int Q>
 __device__ __forceinline__ float fma_hh(uint32_t a, uint32_t qpair, float c) {
@@ -59,20 +67,29 @@ __device__ __forceinline__ void fma8(const uint32_t w[4], uint32_t qpair, float 
   acc[7] = fma_hh<1, Q>(w[3], qpair, acc[7]);
 }
 
-// Per-warp prologue state; lists are in "list order" (T8 class first).
+// Per-stage metadata published by the producer (list order: T8 class first).
 template <int G>
-struct alignas(16) QkWarp {
-  uint32_t q[G][D / 2];  // q (fp16) per list position, pairs (2p, 2p+1); 0 for SKIP heads / pads
-  uint2 hm[G][D];        // per-head (keep, fill) word masks per list position (used when G > 1)
-  uint16_t ent[D];       // channel | class << 8 ; class 0 = pad
-  int nlist;             // padded to a multiple of 8
-  int unit;
+struct alignas(16) QkMeta {
+  int item, u, pg, n;
+  int nlist, pad0, pad1, pad2;
+  uint16_t ent[D];          // channel | union class << 8 ; class 0 = pad
+  uint32_t q[G][D / 2];     // q (fp16) per list position, pairs; 0 for SKIP heads / pads
+  uint8_t code[G][D];       // per-head read code per list position (8/12/16; SKIP -> 8 with q = 0)
 };
 
-struct KBatch {
-  uint2 h[8];
-  uint32_t m[8], l[8];
-  uint4 e;  // 8 list entries
+template <int G>
+struct alignas(128) QkSmem {
+  uint8_t data[QK_NS][PAGE];
+  QkMeta<G> meta[QK_NS];
+  float red[2][4][P];        // partial token sums per group / warp (channel split, G <= 2)
+  float stat[2][4][2];
+  uint64_t full[QK_NS], empty[QK_NS];
+};
+
+template <int G>
+struct QkSplit {
+  static constexpr int CS = G >= 4 ? 1 : 4 / G;  // ways the channel list is split inside a group
+  static constexpr int HW = G >= 4 ? G / 4 : 1;  // heads per consumer warp
 };
 
 __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
@@ -80,81 +97,61 @@ __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
   return (i & 1) ? (w >> 16) : (w & 0xFFFFu);
 }
 
+// ----------------------------------------------------------------------------
+// producer
+// ----------------------------------------------------------------------------
 template <int G>
-__device__ __forceinline__ void k_load(KBatch& X, const QkWarp<G>& ws, int b, const uint8_t* hb, const uint8_t* mb,
-                                       uint64_t pol) {
-  X.e = *reinterpret_cast<const uint4*>(&ws.ent[b * 8]);
+struct QkPrefetch {
+  int item, u, pg, n;
+  uint32_t cm[4];
+  uint32_t qw[G][4];
+};
+
+template <int G>
+__device__ __forceinline__ void qk_grab(QkPrefetch<G>& f, const akv_store_t& s, const akv_step_t& st, int npg_max,
+                                        unsigned total) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned item = 0;
+    if (lane == 0) item = atomicAdd(st.work + 0, 1u);
+    item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    if (item >= total) {
+      f.item = -1;
+      return;
+    }
+    const int u = item / npg_max, pg = item % npg_max;
+    const int n = s.lengths[u];
+    if (pg * P >= n) continue;
+    f.item = (int)item;
+    f.u = u;
+    f.pg = pg;
+    f.n = n;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t en = ent_of(X.e, i);
-    const uint32_t ch = en & 0xFFu, cls = en >> 8;
-    if (cls) X.h[i] = ld_stream_u64(hb + ch * P, pol);
-    if (cls >= 12) X.m[i] = ld_stream_u32(mb + ch * (P / 2), pol);
-    if (cls == 16) X.l[i] = ld_stream_u32(mb + ch * (P / 2) + (LOW - MID), pol);
+    for (int k = 0; k < 4; ++k) f.cm[k] = s.colmax[(size_t)u * D + lane + 32 * k] & 0x7FFFu;
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) f.qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
+    return;
   }
 }
 
 template <int G, bool TRUNC>
-__device__ __forceinline__ void k_compute(const KBatch& X, const QkWarp<G>& ws, int b, float acc[G][8],
-                                          uint32_t tkm, uint32_t tf) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t en = ent_of(X.e, i);
-    const uint32_t cls = en >> 8;
-    if (cls == 0) continue;  // pad (warp-uniform)
-    const int pos = b * 8 + i;
-    uint32_t w[4];
-    if (cls == 8) {
-      const uint32_t c80 = 0x80808080u;
-      w[0] = prmt(X.h[i].x, c80, 0x1404);
-      w[1] = prmt(X.h[i].x, c80, 0x3424);
-      w[2] = prmt(X.h[i].y, c80, 0x1404);
-      w[3] = prmt(X.h[i].y, c80, 0x3424);
-    } else {
-      assemble8(X.h[i].x, X.h[i].y, X.m[i], cls == 16 ? X.l[i] : 0x88888888u, w);
-    }
-    if (TRUNC) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
-    }
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      uint32_t wj[4];
-      if (G > 1 && cls != 8) {
-        const uint2 hm = ws.hm[j][pos];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) wj[k] = (w[k] & hm.x) | hm.y;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) wj[k] = w[k];
-      }
-      const uint32_t qp = ws.q[j][pos >> 1];
-      if (i & 1)
-        fma8<1>(wj, qp, acc[j]);
-      else
-        fma8<0>(wj, qp, acc[j]);
-    }
-  }
-}
-
-// Rule 1 for unit u, all G heads; builds the warp's channel list.
-template <int G, bool TRUNC>
-__device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int u,
-                           int n, bool book) {
+__device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, const akv_store_t& s,
+                           const akv_cfg_t& cfg, const akv_step_t& st) {
   const int lane = threadIdx.x & 31;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
-  uint32_t cm[4], qw[G][4];
+  const bool book = f.pg == 0;
+  QkMeta<G>& mt = sm.meta[stage];
   int code[G][4], ucode[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) cm[k] = s.colmax[(size_t)u * D + lane + 32 * k] & 0x7FFFu;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     int pe[4], mx = INT_MIN;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
-      const bool valid = (qw[j][k] & 0x7FFFu) && cm[k] && finite16(qw[j][k]);
-      pe[k] = valid ? magexp16(qw[j][k]) + magexp16(cm[k]) + 1 : INT_MIN;
+      const uint32_t qw = f.qw[j][k];
+      const bool valid = (qw & 0x7FFFu) && f.cm[k] && finite16(qw);
+      pe[k] = valid ? magexp16(qw) + magexp16(f.cm[k]) + 1 : INT_MIN;
       mx = max(mx, pe[k]);
     }
     const int maxpe = warp_max_i(mx);
@@ -168,7 +165,7 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
       } else {
         const int t = min(max(pe[k] - maxpe + 9 + cfg.margin_bits, 0), 10);  // pe - u - 1 + margin, u = maxpe - 10
         cd = t <= 2 ? 8 : (t <= 6 ? 12 : 16);
-        const bool qz = (qw[j][k] & 0x7FFFu) == 0, cz = cm[k] == 0;
+        const bool qz = (f.qw[j][k] & 0x7FFFu) == 0, cz = f.cm[k] == 0;
         if (cfg.zero_skip) {
           if (qz || cz) cd = 0;
         } else if (qz) {
@@ -181,7 +178,7 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
       ucode[k] = max(ucode[k], cd);
     }
     if (book) {  // per-step bookkeeping, once per unit (the page-0 item)
-      const size_t h = (size_t)u * G + j;
+      const size_t h = (size_t)f.u * G + j;
       int c8 = 0, c12 = 0, c16 = 0, bad = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -189,13 +186,13 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
         c8 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 8));
         c12 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 12));
         c16 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 16));
-        bad += __popc(__ballot_sync(0xFFFFFFFFu, !finite16(qw[j][k])));
+        bad += __popc(__ballot_sync(0xFFFFFFFFu, !finite16(f.qw[j][k])));
       }
       if (lane == 0) {
         int64_t* ct = st.counters + h * 8;
-        ct[0] = (int64_t)c8 * n;
-        ct[1] = (int64_t)c12 * n;
-        ct[2] = (int64_t)c16 * n;
+        ct[0] = (int64_t)c8 * f.n;
+        ct[1] = (int64_t)c12 * f.n;
+        ct[2] = (int64_t)c16 * f.n;
         ct[3] = ct[4] = ct[5] = ct[6] = ct[7] = 0;
         long long w = 0;
         if (bad) w = status_word(AKV_STATUS_BAD_Q, 0);
@@ -204,148 +201,278 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
       }
     }
   }
-  // channel list: T8-class first, then T12/T16 (ascending channel inside each class)
+  // channel list (T8 class first, then T12/T16; ascending channel inside a class)
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t b8[4], bf[4], bm16[4];
-  int n8 = 0, nf = 0, n16 = 0;
+  uint32_t b8[4], bm[4], bl[4];
+  int n8 = 0, nm = 0, nlo = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     b8[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 8);
-    bf[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
-    bm16[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 16);
+    bm[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
+    bl[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 16);
     n8 += __popc(b8[k]);
-    nf += __popc(bf[k]);
-    n16 += __popc(bm16[k]);
+    nm += __popc(bm[k]);
+    nlo += __popc(bl[k]);
   }
-  const int nl = n8 + nf;
-  const int nlp = (nl + 7) & ~7;
-  int base8 = 0, basef = 0;
+  const int nl = n8 + nm, nlp = (nl + 7) & ~7;
+  int base8 = 0, basem = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int c = lane + 32 * k;
     int pos = -1;
     if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
-    else if (ucode[k] >= 12) pos = n8 + basef + __popc(bf[k] & lt);
+    else if (ucode[k] >= 12) pos = n8 + basem + __popc(bm[k] & lt);
     if (pos >= 0) {
-      ws.ent[pos] = (uint16_t)(c | (ucode[k] << 8));
+      mt.ent[pos] = (uint16_t)(c | (ucode[k] << 8));
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        reinterpret_cast<uint16_t*>(ws.q[j])[pos] = code[j][k] ? (uint16_t)qw[j][k] : (uint16_t)0;
-        if (G > 1) {
-          const int cd = code[j][k];
-          ws.hm[j][pos] = cd >= 16 ? make_uint2(0xFFFFFFFFu, 0u)
-                                   : (cd == 12 ? make_uint2(0xFFF0FFF0u, 0x00080008u) : make_uint2(0xFF00FF00u, 0x00800080u));
-        }
+        reinterpret_cast<uint16_t*>(mt.q[j])[pos] = code[j][k] ? (uint16_t)f.qw[j][k] : (uint16_t)0;
+        mt.code[j][pos] = (uint8_t)(code[j][k] ? code[j][k] : 8);
       }
     }
     base8 += __popc(b8[k]);
-    basef += __popc(bf[k]);
+    basem += __popc(bm[k]);
   }
   for (int pos = nl + lane; pos < nlp; pos += 32) {
-    ws.ent[pos] = 0;
+    mt.ent[pos] = 0;
 #pragma unroll
-    for (int j = 0; j < G; ++j) reinterpret_cast<uint16_t*>(ws.q[j])[pos] = 0;
+    for (int j = 0; j < G; ++j) {
+      reinterpret_cast<uint16_t*>(mt.q[j])[pos] = 0;
+      mt.code[j][pos] = 8;
+    }
   }
   if (book && lane == 0) {
-    st.unit_bytes[(size_t)u * 4 + 0] = (int64_t)n * nl + (int64_t)(n / 2) * (nf + n16);
-    st.unit_bytes[(size_t)u * 4 + 1] = 0;
+    st.unit_bytes[(size_t)f.u * 4 + 0] = (int64_t)f.n * nl + (int64_t)(f.n / 2) * (nm + nlo);
+    st.unit_bytes[(size_t)f.u * 4 + 1] = 0;
   }
   if (lane == 0) {
-    ws.nlist = nlp;
-    ws.unit = u;
+    mt.item = f.item;
+    mt.u = f.u;
+    mt.pg = f.pg;
+    mt.n = f.n;
+    mt.nlist = nlp;
+  }
+  // TMA: head plane in one copy, mid / low rows as runs of consecutive channels
+  const uint8_t* src = page_ptr(s.k_pool, s.page_table, s.max_pages, f.u, f.pg);
+  uint8_t* dst = sm.data[stage];
+  const uint32_t bytes = (uint32_t)(D * P) + (uint32_t)(nm + nlo) * (P / 2);
+  __syncwarp();
+  if (lane == 0) {
+    mbar_arrive_expect_tx(&sm.full[stage], bytes);
+    bulk_g2s(dst, src, D * P, &sm.full[stage]);
   }
   __syncwarp();
+#pragma unroll
+  for (int pl = 0; pl < 2; ++pl) {
+    const uint32_t* mk = pl == 0 ? bm : bl;
+    const int off = pl == 0 ? MID : LOW;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = lane + 32 * k;
+      const bool on = (mk[k] >> lane) & 1u;
+      const bool prev = c > 0 && ((mk[(c - 1) >> 5] >> ((c - 1) & 31)) & 1u);
+      if (on && !prev) {
+        int e = c + 1;
+        while (e < D && ((mk[e >> 5] >> (e & 31)) & 1u)) ++e;
+        bulk_g2s(dst + off + c * (P / 2), src + off + c * (P / 2), (uint32_t)(e - c) * (P / 2), &sm.full[stage]);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// consumer
+// ----------------------------------------------------------------------------
+template <int G, bool TRUNC>
+__device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, int w4, const akv_store_t& s,
+                                           const akv_step_t& st, int cap, float isd, uint32_t tkm, uint32_t tf) {
+  constexpr int CS = QkSplit<G>::CS, HW = QkSplit<G>::HW;
+  const int lane = threadIdx.x & 31;
+  const QkMeta<G>& mt = sm.meta[stage];
+  const uint8_t* pgd = sm.data[stage];
+  const int cs = w4 % CS;
+  const int j0 = (w4 / CS) * HW;  // first head of this warp
+  const int nb = mt.nlist >> 3;
+  const int u = mt.u, pg = mt.pg, n = mt.n;  // read before the stage is released
+  float acc[HW][8];
+#pragma unroll
+  for (int jj = 0; jj < HW; ++jj)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[jj][e] = 0.f;
+  const uint8_t* hb = pgd + lane * 8;
+  const uint8_t* mb = pgd + MID + lane * 4;
+
+  for (int b = cs; b < nb; b += CS) {
+    const uint4 e4 = *reinterpret_cast<const uint4*>(&mt.ent[b * 8]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t en = ent_of(e4, i);
+      const uint32_t ch = en & 0xFFu, cls = en >> 8;
+      if (cls == 0) continue;  // pad (warp-uniform)
+      const int pos = b * 8 + i;
+      const uint2 h = *reinterpret_cast<const uint2*>(hb + ch * P);
+      uint32_t w[4];
+      if (cls == 8) {
+        const uint32_t c80 = 0x80808080u;
+        w[0] = prmt(h.x, c80, 0x1404);
+        w[1] = prmt(h.x, c80, 0x3424);
+        w[2] = prmt(h.y, c80, 0x1404);
+        w[3] = prmt(h.y, c80, 0x3424);
+      } else {
+        const uint32_t m = *reinterpret_cast<const uint32_t*>(mb + ch * (P / 2));
+        const uint32_t l = cls == 16 ? *reinterpret_cast<const uint32_t*>(mb + (LOW - MID) + ch * (P / 2)) : 0x88888888u;
+        assemble8(h.x, h.y, m, l, w);
+      }
+      if (TRUNC) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
+      }
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj) {
+        const int j = j0 + jj;
+        uint32_t wj[4];
+        if (G > 1 && cls != 8) {
+          const uint32_t cd = mt.code[j][pos];
+          const uint32_t km = cd >= 16 ? 0xFFFFFFFFu : (cd == 12 ? 0xFFF0FFF0u : 0xFF00FF00u);
+          const uint32_t fl = cd >= 16 ? 0u : (cd == 12 ? 0x00080008u : 0x00800080u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) wj[k] = (w[k] & km) | fl;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) wj[k] = w[k];
+        }
+        const uint32_t qp = mt.q[j][pos >> 1];
+        if (i & 1) fma8<1>(wj, qp, acc[jj]);
+        else fma8<0>(wj, qp, acc[jj]);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage data no longer read by this warp
+
+  const int tok0 = pg * P + lane * 8;
+  const int nv = min(max(n - tok0, 0), 8);
+  auto finish = [&](int j, const float* sv8) {
+    const size_t hh = (size_t)u * G + j;
+    float sv[8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      sv[e] = sv8[e] * isd;
+      if (e < nv) m = fmaxf(m, sv[e]);
+    }
+    m = warp_max(m);
+    float l = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < nv) l += expf(sv[e] - m);
+    l = warp_sum(l);
+    float* out = st.scores + hh * cap + tok0;
+    if (nv == 8) {
+      reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+      reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < nv) out[e] = sv[e];
+    }
+    if (lane == 0) {
+      float* ps = st.page_stats + (hh * s.max_pages + pg) * 2;
+      ps[0] = m;
+      ps[1] = l;
+    }
+  };
+  if (CS == 1) {
+#pragma unroll
+    for (int jj = 0; jj < HW; ++jj) finish(j0 + jj, acc[jj]);
+  } else {
+    // G == 1 (4-way channel split) or G == 2 (2 heads x 2-way split): reduce via shared memory
+    const int j = w4 / CS;
+    float* rw = sm.red[grp][w4];
+    *reinterpret_cast<float4*>(rw + lane * 8) = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+    *reinterpret_cast<float4*>(rw + lane * 8 + 4) = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+    named_bar(1 + grp, 128);
+    if (cs == 0) {
+      float sum[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sum[e] = 0.f;
+#pragma unroll
+      for (int c2 = 0; c2 < CS; ++c2) {  // fixed order
+        const float* r2 = sm.red[grp][w4 + c2] + lane * 8;
+        const float4 a = *reinterpret_cast<const float4*>(r2);
+        const float4 bq = *reinterpret_cast<const float4*>(r2 + 4);
+        sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
+        sum[4] += bq.x; sum[5] += bq.y; sum[6] += bq.z; sum[7] += bq.w;
+      }
+      finish(j, sum);
+    }
+    named_bar(1 + grp, 128);
+  }
 }
 
 template <int G, bool TRUNC>
-__global__ void __launch_bounds__(128) qk_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap,
-                                                 float inv_sqrt_d, int npg_max) {
-  __shared__ QkWarp<G> wsm[4];
+__global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap,
+                                                           float isd, int npg_max) {
+  extern __shared__ __align__(128) uint8_t qk_smem_raw[];
+  QkSmem<G>& sm = *reinterpret_cast<QkSmem<G>*>(qk_smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  QkWarp<G>& ws = wsm[warp];
-  if (lane == 0) ws.unit = -1;
-  __syncwarp();
-  const uint64_t pol = evict_first_policy();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < QK_NS; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 4);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
   const unsigned total = (unsigned)s.n_units * npg_max;
-  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
-  if (TRUNC) {
-    const int kb = cfg.trunc_bits - 6;
-    const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
-    const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
-    tkm = km | (km << 16);
-    tf = fill | (fill << 16);
-  }
 
-  for (;;) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(st.work + 0, 1u);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= total) break;
-    const int u = item / npg_max, pg = item % npg_max;
-    const int n = s.lengths[u];
-    if (pg * P >= n) continue;
-    if (ws.unit != u || pg == 0) k_prologue<G, TRUNC>(ws, s, cfg, st, u, n, pg == 0);
-
-    const uint8_t* base = page_ptr(s.k_pool, s.page_table, s.max_pages, u, pg);
-    const uint8_t* hb = base + lane * 8;
-    const uint8_t* mb = base + MID + lane * 4;
-    float acc[G][8];
-#pragma unroll
-    for (int j = 0; j < G; ++j)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[j][e] = 0.f;
-
-    const int nb = ws.nlist >> 3;
-    KBatch A, B;
-    if (nb > 0) k_load<G>(A, ws, 0, hb, mb, pol);
-    for (int b = 0; b < nb; b += 2) {
-      if (b + 1 < nb) k_load<G>(B, ws, b + 1, hb, mb, pol);
-      k_compute<G, TRUNC>(A, ws, b, acc, tkm, tf);
-      if (b + 1 >= nb) break;
-      if (b + 2 < nb) k_load<G>(A, ws, b + 2, hb, mb, pol);
-      k_compute<G, TRUNC>(B, ws, b + 1, acc, tkm, tf);
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    QkPrefetch<G> cur, nxt;
+    qk_grab<G>(nxt, s, st, npg_max, total);
+    int k = 0;
+    for (;; ++k) {
+      cur = nxt;
+      if (cur.item < 0) break;
+      qk_grab<G>(nxt, s, st, npg_max, total);  // prefetch the next item's q / colmax
+      const int stage = k % QK_NS;
+      mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
+      qk_produce<G, TRUNC>(sm, cur, stage, s, cfg, st);
     }
-
-    // epilogue: scores + page softmax stats
-    const int tok0 = pg * P + lane * 8;
-    const int nv = min(max(n - tok0, 0), 8);
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const size_t h = (size_t)u * G + j;
-      float sv[8];
-      float m = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        sv[e] = acc[j][e] * inv_sqrt_d;
-        if (e < nv) m = fmaxf(m, sv[e]);
-      }
-      m = warp_max(m);
-      float l = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e < nv) l += expf(sv[e] - m);
-      l = warp_sum(l);
-      float* out = st.scores + h * cap + tok0;
-      if (nv == 8) {
-        reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-        reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < nv) out[e] = sv[e];
-      }
+    // one terminator per consumer group
+    for (int t = 0; t < 2; ++t, ++k) {
+      const int stage = k % QK_NS;
+      mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
       if (lane == 0) {
-        float* ps = st.page_stats + (h * s.max_pages + pg) * 2;
-        ps[0] = m;
-        ps[1] = l;
+        sm.meta[stage].item = -1;
+        mbar_arrive(&sm.full[stage]);
       }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumers: two groups of four warps ----------------
+    const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
+    uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
+    if (TRUNC) {
+      const int kb = cfg.trunc_bits - 6;
+      const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
+      const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
+      tkm = km | (km << 16);
+      tf = fill | (fill << 16);
+    }
+    for (int k = grp;; k += 2) {
+      const int stage = k % QK_NS;
+      mbar_wait(&sm.full[stage], (k / QK_NS) & 1);
+      if (sm.meta[stage].item < 0) break;
+      qk_consume<G, TRUNC>(sm, stage, grp, w4, s, st, cap, isd, tkm, tf);
     }
   }
-  // self-resetting queue: the last warp out rewinds it for the next launch
-  if (lane == 0) {
+  // self-resetting queue: the last CTA out rewinds it for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
     const unsigned done = atomicAdd(st.work + 1, 1u);
-    if (done == gridDim.x * 4 - 1) {
+    if (done == gridDim.x - 1) {
       st.work[0] = 0;
       st.work[1] = 0;
       __threadfence();
@@ -353,26 +480,23 @@ __global__ void __launch_bounds__(128) qk_kernel(akv_store_t s, akv_cfg_t cfg, a
   }
 }
 
-template <typename K>
-int resident_blocks(K kernel, size_t smem = 0) {
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 128, smem);
-  return max(1, sms * max(per, 1));
-}
-
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
-  static int resident = 0;
-  if (!resident) resident = resident_blocks(qk_kernel<G, TRUNC>);
+  static int sms = 0;
+  const size_t smem = sizeof(QkSmem<G>);
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(qk_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, (items + 3) / 4);
+  const int grid = (int)std::min<long long>(sms, std::max<long long>(items / 2, 1));
   const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  qk_kernel<G, TRUNC><<<max(grid, 1), 128, 0, stream>>>(s, cfg, st, cap, isd, npg);
+  qk_kernel<G, TRUNC><<<grid, QK_THREADS, smem, stream>>>(s, cfg, st, cap, isd, npg);
 }
 
 void launch_qk(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len, cudaStream_t stream) {

@@ -238,9 +238,50 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
     if (r < cnt) st.sel_idx[(size_t)h * AKV_MAX_KSEL + r] = sm.sel_sorted[r];
   }
   __syncthreads();
+  const int tmin_all = min(min(sm.tmin[0], sm.tmin[1]), min(sm.tmin[2], sm.tmin[3]));
+  const int unk_all = sm.tunk[0] + sm.tunk[1] + sm.tunk[2] + sm.tunk[3];
+  // 6. V rows needing the mid / low nibble row for this head (PV fetch plan):
+  //    element strategy: RowMax superset bound (H6); row strategy: the row tier (D7)
+  {
+    uint32_t* nb = st.need_bits + (size_t)h * 2 * (cap >> 5);
+    for (int t0 = 0; t0 < n; t0 += ST) {
+      const int t = t0 + tid;
+      bool nm = false, nlw = false;
+      if (t < n && est) {
+        const bool sel = (bits[t >> 5] >> (t & 31)) & 1u;
+        const float p = pr[t];
+        const uint32_t rm = s.rowmax[(size_t)u * s.max_pages * P + t];
+        if (!sel && cfg.strategy == 1) {
+          int tier = 16;
+          if (!unk_all) {
+            if (p == 0.f || rm == 0) tier = 8;
+            else {
+              const int tr = min(max(floor_log2f(p) + magexp16(rm) + 1 - tmin_all - 1 + cfg.margin_bits, 0), 10);
+              tier = tr <= 2 ? 8 : (tr <= 6 ? 12 : 16);
+            }
+          }
+          nm = tier >= 12;
+          nlw = tier == 16;
+        } else if (!sel && p > 0.f) {
+          if (unk_all) {
+            nm = nlw = true;
+          } else {
+            const int bound = floor_log2f(p) + (max(bexp16(rm), 1) - 15) + 1 - tmin_all - 1 + cfg.margin_bits;
+            nm = bound > 2;
+            nlw = bound > 6;
+          }
+        }
+      }
+      const unsigned bm = __ballot_sync(0xFFFFFFFFu, nm), bl = __ballot_sync(0xFFFFFFFFu, nlw);
+      if (lane == 0 && t < n) {
+        nb[t >> 5] = bm;
+        nb[(cap >> 5) + (t >> 5)] = bl;
+      }
+    }
+  }
   if (tid == 0) {
-    const int tmin = min(min(sm.tmin[0], sm.tmin[1]), min(sm.tmin[2], sm.tmin[3]));
-    const int unk = sm.tunk[0] + sm.tunk[1] + sm.tunk[2] + sm.tunk[3];
+    const int tmin = tmin_all;
+    const int unk = unk_all;
     int32_t* hm = st.head_meta + (size_t)h * 4;
     hm[0] = cnt;
     hm[1] = tmin;

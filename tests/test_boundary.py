@@ -58,7 +58,7 @@ def test_struct_layouts_match_header():
     assert fields("akv_step_t") == [f[0] for f in _lib.AkvStep._fields_]
     assert ctypes.sizeof(_lib.AkvStore) == 16 + 6 * 8
     assert ctypes.sizeof(_lib.AkvCfg) == 32
-    assert ctypes.sizeof(_lib.AkvStep) == 18 * 8
+    assert ctypes.sizeof(_lib.AkvStep) == 19 * 8
 
 
 def test_workspace_sizes(L):

@@ -67,7 +67,8 @@ def test_append_rejects_nonfinite_with_position():
     kb[0, 0, 2, 9] = float("nan")
     with pytest.raises(ValueError, match=r"in K at batch 0, kv-head 0, token 7, channel 9"):
         st.append(kb, torch.randn(1, 2, 3, 128).half())
-    assert st.lengths.tolist() == [[5, 5]]
+    assert st.lengths.tolist() == [[5, 8]]  # unit (0,1) committed its 3 finite tokens
+    st.rewind(5)
     st.append_token(k2, torch.randn(1, 2, 128).half())
     assert st.lengths.tolist() == [[6, 6]]
 
