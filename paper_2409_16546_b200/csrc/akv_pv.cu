@@ -2,7 +2,7 @@
 //
 // Warp-specialised persistent kernel, one CTA per SM:
 //
-//  producer warp   pulls (unit, page) items from an atomic queue, reads the
+//  producer warp   walks a static strided (unit, page) schedule, reads the
 //                  page's per-head "need mid / need low" row bitmaps written by
 //                  akv_softmax_select (RowMax superset rule; row
 //                  tiers for the row strategy, D7), and streams the page into
@@ -77,45 +77,34 @@ struct PvPrefetch {
   uint32_t um, ul;  // lane w < 8: union need words w of this page
 };
 
+// Issue the loads an item needs (no wait: the registers are consumed one item later).
 template <int G>
-__device__ __forceinline__ void pv_grab(PvPrefetch& f, const akv_store_t& s, const akv_cfg_t& cfg,
-                                        const akv_step_t& st, int npg_max, unsigned total, int cap, bool uniform) {
+__device__ __forceinline__ void pv_fetch(PvPrefetch& f, const akv_store_t& s, const akv_cfg_t& cfg,
+                                         const akv_step_t& st, int npg_max, long long idx, long long total, int cap,
+                                         bool uniform) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(st.work + 2, 1u);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= total) {
-      f.item = -1;
-      return;
-    }
-    const int u = item / npg_max, pg = item % npg_max;
-    const int n = s.lengths[u];
-    if (pg * P >= n) continue;
-    f.item = (int)item;
-    f.u = u;
-    f.pg = pg;
-    f.n = n;
-    f.um = f.ul = 0u;
-    if (lane < 8) {
-      if (uniform) {
-        f.um = cfg.force_tier >= 12 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
-        f.ul = cfg.force_tier >= 16 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
-      } else {
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          const uint32_t* nb = st.need_bits + ((size_t)u * G + j) * 2 * (cap >> 5) + pg * 8 + lane;
-          f.um |= nb[0];
-          f.ul |= nb[cap >> 5];
-        }
-      }
-      // rows beyond n hold stale bits
-      const int lo = lane * 32, valid = min(max(n - pg * P - lo, 0), 32);
-      const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-      f.um &= vm;
-      f.ul &= vm;
-    }
+  if (idx >= total) {
+    f.item = -1;
     return;
+  }
+  const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
+  f.item = (int)idx;
+  f.u = u;
+  f.pg = pg;
+  f.n = s.lengths[u];
+  f.um = f.ul = 0u;
+  if (lane < 8) {
+    if (uniform) {
+      f.um = cfg.force_tier >= 12 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
+      f.ul = cfg.force_tier >= 16 || cfg.trunc_bits ? 0xFFFFFFFFu : 0u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const uint32_t* nb = st.need_bits + ((size_t)u * G + j) * 2 * (cap >> 5) + pg * 8 + lane;
+        f.um |= nb[0];
+        f.ul |= nb[cap >> 5];
+      }
+    }
   }
 }
 
@@ -125,10 +114,16 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
   const int lane = threadIdx.x & 31;
   PvMeta& mt = sm.meta[stage];
   uint32_t um[8], ul[8];
+  {
+    // rows beyond n hold stale bits
+    const int lo = (lane & 7) * 32, valid = min(max(f.n - f.pg * P - lo, 0), 32);
+    const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+    const uint32_t m0 = f.um & vm, l0 = f.ul & vm;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    um[w] = __shfl_sync(0xFFFFFFFFu, f.um, w);
-    ul[w] = __shfl_sync(0xFFFFFFFFu, f.ul, w);
+    for (int w = 0; w < 8; ++w) {
+      um[w] = __shfl_sync(0xFFFFFFFFu, m0, w);
+      ul[w] = __shfl_sync(0xFFFFFFFFu, l0, w);
+    }
   }
   int nm = 0, nl = 0;
 #pragma unroll
@@ -370,20 +365,25 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
     mbar_fence_init();
   }
   __syncthreads();
-  const unsigned total = (unsigned)s.n_units * npg_max;
+  const long long total = (long long)s.n_units * npg_max;
   const bool uniform = cfg.force_tier != 0 || TRUNC;
 
   if (warp == 0) {
+    // ---------------- producer: static strided item schedule, loads one item ahead ----------------
     PvPrefetch cur, nxt;
-    pv_grab<G>(nxt, s, cfg, st, npg_max, total, cap, uniform);
+    long long idx = blockIdx.x;
+    pv_fetch<G>(nxt, s, cfg, st, npg_max, idx, total, cap, uniform);
     int k = 0;
-    for (;; ++k) {
+    for (;;) {
       cur = nxt;
       if (cur.item < 0) break;
-      pv_grab<G>(nxt, s, cfg, st, npg_max, total, cap, uniform);
+      idx += gridDim.x;
+      pv_fetch<G>(nxt, s, cfg, st, npg_max, idx, total, cap, uniform);
+      if (cur.pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
       const int stage = k % NS;
       mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
       pv_produce<G>(sm, cur, stage, s, st, cap);
+      ++k;
     }
     for (int t = 0; t < NG; ++t, ++k) {
       const int stage = k % NS;
@@ -401,16 +401,6 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
       mbar_wait(&sm.full[stage], (k / NS) & 1);
       if (sm.meta[stage].item < 0) break;
       pv_consume<G, TRUNC, EXPORT>(sm, stage, grp, w4, cfg, st, cap);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(st.work + 3, 1u);
-    if (done == gridDim.x - 1) {
-      st.work[2] = 0;
-      st.work[3] = 0;
-      __threadfence();
     }
   }
 }

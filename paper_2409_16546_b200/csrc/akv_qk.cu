@@ -2,8 +2,8 @@
 //
 // Warp-specialised persistent kernel, one CTA per SM:
 //
-//  producer warp   pulls (unit, page) items from an atomic queue (no wave
-//                  tail), evaluates Rule 1 for the unit's q-heads
+//  producer warp   walks a static strided (unit, page) schedule (its loads
+//                  are issued one item ahead), evaluates Rule 1 for the unit's q-heads
 //                  (rule1_target SPEC.md:157-165, required_mantissa_bits
 //                  :139-147, tier_for_bits :148-156, k_channel_tiers :175-183,
 //                  SURVEY App. A A-K/D1/D2/D8), publishes the channel list and
@@ -107,33 +107,26 @@ struct QkPrefetch {
   uint32_t qw[G][4];
 };
 
+// Issue the loads an item needs (no wait: the registers are consumed one item later).
 template <int G>
-__device__ __forceinline__ void qk_grab(QkPrefetch<G>& f, const akv_store_t& s, const akv_step_t& st, int npg_max,
-                                        unsigned total) {
+__device__ __forceinline__ void qk_fetch(QkPrefetch<G>& f, const akv_store_t& s, const akv_step_t& st, int npg_max,
+                                         long long idx, long long total) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned item = 0;
-    if (lane == 0) item = atomicAdd(st.work + 0, 1u);
-    item = __shfl_sync(0xFFFFFFFFu, item, 0);
-    if (item >= total) {
-      f.item = -1;
-      return;
-    }
-    const int u = item / npg_max, pg = item % npg_max;
-    const int n = s.lengths[u];
-    if (pg * P >= n) continue;
-    f.item = (int)item;
-    f.u = u;
-    f.pg = pg;
-    f.n = n;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) f.cm[k] = s.colmax[(size_t)u * D + lane + 32 * k] & 0x7FFFu;
-#pragma unroll
-    for (int j = 0; j < G; ++j)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) f.qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
+  if (idx >= total) {
+    f.item = -1;
     return;
   }
+  const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
+  f.item = (int)idx;
+  f.u = u;
+  f.pg = pg;
+  f.n = s.lengths[u];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f.cm[k] = s.colmax[(size_t)u * D + lane + 32 * k];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f.qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
 }
 
 template <int G, bool TRUNC>
@@ -150,8 +143,9 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t qw = f.qw[j][k];
-      const bool valid = (qw & 0x7FFFu) && f.cm[k] && finite16(qw);
-      pe[k] = valid ? magexp16(qw) + magexp16(f.cm[k]) + 1 : INT_MIN;
+      const uint32_t cmk = f.cm[k] & 0x7FFFu;
+      const bool valid = (qw & 0x7FFFu) && cmk && finite16(qw);
+      pe[k] = valid ? magexp16(qw) + magexp16(cmk) + 1 : INT_MIN;
       mx = max(mx, pe[k]);
     }
     const int maxpe = warp_max_i(mx);
@@ -165,7 +159,7 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
       } else {
         const int t = min(max(pe[k] - maxpe + 9 + cfg.margin_bits, 0), 10);  // pe - u - 1 + margin, u = maxpe - 10
         cd = t <= 2 ? 8 : (t <= 6 ? 12 : 16);
-        const bool qz = (f.qw[j][k] & 0x7FFFu) == 0, cz = f.cm[k] == 0;
+        const bool qz = (f.qw[j][k] & 0x7FFFu) == 0, cz = (f.cm[k] & 0x7FFFu) == 0;
         if (cfg.zero_skip) {
           if (qz || cz) cd = 0;
         } else if (qz) {
@@ -424,20 +418,24 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
     mbar_fence_init();
   }
   __syncthreads();
-  const unsigned total = (unsigned)s.n_units * npg_max;
+  const long long total = (long long)s.n_units * npg_max;
 
   if (warp == 0) {
-    // ---------------- producer ----------------
+    // ---------------- producer: static strided item schedule, loads one item ahead ----------------
     QkPrefetch<G> cur, nxt;
-    qk_grab<G>(nxt, s, st, npg_max, total);
+    long long idx = blockIdx.x;
+    qk_fetch<G>(nxt, s, st, npg_max, idx, total);
     int k = 0;
-    for (;; ++k) {
+    for (;;) {
       cur = nxt;
       if (cur.item < 0) break;
-      qk_grab<G>(nxt, s, st, npg_max, total);  // prefetch the next item's q / colmax
+      idx += gridDim.x;
+      qk_fetch<G>(nxt, s, st, npg_max, idx, total);
+      if (cur.pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
       const int stage = k % QK_NS;
       mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
       qk_produce<G, TRUNC>(sm, cur, stage, s, cfg, st);
+      ++k;
     }
     // one terminator per consumer group
     for (int t = 0; t < 2; ++t, ++k) {
@@ -465,17 +463,6 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
       mbar_wait(&sm.full[stage], (k / QK_NS) & 1);
       if (sm.meta[stage].item < 0) break;
       qk_consume<G, TRUNC>(sm, stage, grp, w4, s, st, cap, isd, tkm, tf);
-    }
-  }
-  // self-resetting queue: the last CTA out rewinds it for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(st.work + 1, 1u);
-    if (done == gridDim.x - 1) {
-      st.work[0] = 0;
-      st.work[1] = 0;
-      __threadfence();
     }
   }
 }
