@@ -119,6 +119,41 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Issue bulk copies for every run of set bits in an NW-word row mask (all words
+// held in registers by every lane; only compile-time indices touch them, so no
+// local memory).  Lane w < NW owns the runs that start in word w; a run
+// [r0, r1) copies bytes [off + r0*row, off + r1*row) of src into dst.
+template <int NW>
+__device__ __forceinline__ void bulk_runs(const uint32_t (&mk)[NW], uint8_t* dst, const uint8_t* src, int off,
+                                          int row, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  if (lane >= NW) return;
+  uint32_t m = 0, prev = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    if (w == lane) m = mk[w];
+    if (w + 1 == lane) prev = mk[w] >> 31;
+  }
+  uint32_t starts = m & ~((m << 1) | prev);
+  while (starts) {
+    const int sb = __ffs(starts) - 1;
+    starts &= starts - 1;
+    const uint32_t z = ~m & (0xFFFFFFFFu << sb);
+    int e = NW * 32;
+    if (z) {
+      e = lane * 32 + __ffs(z) - 1;
+    } else {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t zz = ~mk[w];
+        if (w > lane && e == NW * 32 && zz) e = w * 32 + __ffs(zz) - 1;
+      }
+    }
+    const int r0 = lane * 32 + sb;
+    bulk_g2s(dst + off + r0 * row, src + off + r0 * row, (uint32_t)(e - r0) * row, bar);
+  }
+}
+
 // Named barrier over `count` threads (ids 1.. are free; 0 is __syncthreads).
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

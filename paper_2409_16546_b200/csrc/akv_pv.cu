@@ -114,16 +114,14 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
   const int lane = threadIdx.x & 31;
   PvMeta& mt = sm.meta[stage];
   uint32_t um[8], ul[8];
-  {
-    // rows beyond n hold stale bits
-    const int lo = (lane & 7) * 32, valid = min(max(f.n - f.pg * P - lo, 0), 32);
-    const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-    const uint32_t m0 = f.um & vm, l0 = f.ul & vm;
+  // rows beyond n hold stale bits
+  const int vlo = (lane & 7) * 32, valid = min(max(f.n - f.pg * P - vlo, 0), 32);
+  const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+  const uint32_t m0 = f.um & vm, l0 = f.ul & vm;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      um[w] = __shfl_sync(0xFFFFFFFFu, m0, w);
-      ul[w] = __shfl_sync(0xFFFFFFFFu, l0, w);
-    }
+  for (int w = 0; w < 8; ++w) {
+    um[w] = __shfl_sync(0xFFFFFFFFu, m0, w);
+    ul[w] = __shfl_sync(0xFFFFFFFFu, l0, w);
   }
   int nm = 0, nl = 0;
 #pragma unroll
@@ -139,8 +137,8 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
     mt.n = f.n;
   }
   if (lane < 8) {
-    mt.un_mid[lane] = um[lane];
-    mt.un_low[lane] = ul[lane];
+    mt.un_mid[lane] = m0;
+    mt.un_low[lane] = l0;
   }
   const uint8_t* src = page_ptr(s.v_pool, s.page_table, s.max_pages, f.u, f.pg);
   uint8_t* dst = sm.data[stage];
@@ -162,18 +160,9 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
     bulk_g2s(ax.need[lane][0], st.need_bits + h * 2 * (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
     bulk_g2s(ax.need[lane][1], st.need_bits + h * 2 * (cap >> 5) + (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
   }
-  // runs of rows needing the mid / low nibble row; lane l scans rows [8l, 8l+8)
-#pragma unroll
-  for (int pl = 0; pl < 2; ++pl) {
-    const uint32_t* mk = pl == 0 ? um : ul;
-    const int off = pl == 0 ? MID : LOW;
-    for (int r = lane * 8; r < lane * 8 + 8; ++r) {
-      if (!bit8(mk, r) || (r > 0 && bit8(mk, r - 1))) continue;
-      int e = r + 1;
-      while (e < P && bit8(mk, e)) ++e;
-      bulk_g2s(dst + off + r * (D / 2), src + off + r * (D / 2), (uint32_t)(e - r) * (D / 2), &sm.full[stage]);
-    }
-  }
+  // runs of rows needing the mid / low nibble row
+  bulk_runs<8>(um, dst, src, MID, D / 2, &sm.full[stage]);
+  bulk_runs<8>(ul, dst, src, LOW, D / 2, &sm.full[stage]);
 }
 
 // ----------------------------------------------------------------------------
@@ -258,7 +247,8 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
         assemble8(h.x, h.y, bsel(tm.mk, mv, 0x88888888u), bsel(tm.lk, lv, tm.lf), w);
         if (aligned && mode != 8) {
           adj[j][0] -= 8;
-          adj[j][mode == 12 ? 1 : 2] += 8;
+          if (mode == 12) adj[j][1] += 8;
+          else adj[j][2] += 8;
         }
         if (EXPORT) clo = chi = (uint32_t)mode * 0x01010101u;
       } else {
@@ -277,10 +267,9 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
           uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
           w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
           w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
-          if (km) {
-            adj[j][0] -= 1;
-            adj[j][kl ? 2 : 1] += 1;
-          }
+          adj[j][0] -= km ? 1 : 0;
+          adj[j][1] += (km && !kl) ? 1 : 0;
+          adj[j][2] += kl ? 1 : 0;
           if (EXPORT) {
             const uint32_t cd = kl ? 16u : (km ? 12u : 8u);
             if (e < 4) clo |= cd << (8 * e);
@@ -309,8 +298,10 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
         nsel += __popc(ax.sel[j][w] & vm);
       }
     }
-    const int slot = aligned ? 0 : (uni == 8 ? 0 : (uni == 12 ? 1 : 2));
-    adj[j][slot] += (rows - nsel) * D;
+    const int base = (rows - nsel) * D;
+    if (aligned || uni == 8) adj[j][0] += base;
+    else if (uni == 12) adj[j][1] += base;
+    else adj[j][2] += base;
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp

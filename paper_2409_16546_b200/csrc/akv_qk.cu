@@ -256,22 +256,8 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     bulk_g2s(dst, src, D * P, &sm.full[stage]);
   }
   __syncwarp();
-#pragma unroll
-  for (int pl = 0; pl < 2; ++pl) {
-    const uint32_t* mk = pl == 0 ? bm : bl;
-    const int off = pl == 0 ? MID : LOW;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = lane + 32 * k;
-      const bool on = (mk[k] >> lane) & 1u;
-      const bool prev = c > 0 && ((mk[(c - 1) >> 5] >> ((c - 1) & 31)) & 1u);
-      if (on && !prev) {
-        int e = c + 1;
-        while (e < D && ((mk[e >> 5] >> (e & 31)) & 1u)) ++e;
-        bulk_g2s(dst + off + c * (P / 2), src + off + c * (P / 2), (uint32_t)(e - c) * (P / 2), &sm.full[stage]);
-      }
-    }
-  }
+  bulk_runs<4>(bm, dst, src, MID, P / 2, &sm.full[stage]);
+  bulk_runs<4>(bl, dst, src, LOW, P / 2, &sm.full[stage]);
 }
 
 // ----------------------------------------------------------------------------
