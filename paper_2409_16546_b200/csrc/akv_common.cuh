@@ -119,38 +119,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-// Issue bulk copies for every run of set bits in an NW-word row mask (all words
-// held in registers by every lane; only compile-time indices touch them, so no
-// local memory).  Lane w < NW owns the runs that start in word w; a run
-// [r0, r1) copies bytes [off + r0*row, off + r1*row) of src into dst.
-template <int NW>
-__device__ __forceinline__ void bulk_runs(const uint32_t (&mk)[NW], uint8_t* dst, const uint8_t* src, int off,
-                                          int row, uint64_t* bar) {
+// 16-byte cp.async (LDGSTS, L2 only) and its completion as an mbarrier arrival.
+// The arrival does not increment the pending count (.noinc): the barrier's
+// init count includes one arrival per producer lane.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Copy the rows of a plane whose bit is set in an NW-word mask: ROW bytes per
+// row (ROW/16 lanes per row, 512/ROW rows per warp instruction); groups of rows
+// with no bit set are skipped (warp-uniform).
+template <int NW, int ROW>
+__device__ __forceinline__ void cp_rows(const uint32_t (&mk)[NW], uint8_t* dst, const uint8_t* src) {
+  constexpr int LPR = ROW / 16, RPI = 32 / LPR;  // lanes per row, rows per instruction
   const int lane = threadIdx.x & 31;
-  if (lane >= NW) return;
-  uint32_t m = 0, prev = 0;
+  const int rsub = lane / LPR, chunk = lane % LPR;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    if (w == lane) m = mk[w];
-    if (w + 1 == lane) prev = mk[w] >> 31;
-  }
-  uint32_t starts = m & ~((m << 1) | prev);
-  while (starts) {
-    const int sb = __ffs(starts) - 1;
-    starts &= starts - 1;
-    const uint32_t z = ~m & (0xFFFFFFFFu << sb);
-    int e = NW * 32;
-    if (z) {
-      e = lane * 32 + __ffs(z) - 1;
-    } else {
+    const uint32_t m = mk[w];
+    if (!m) continue;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t zz = ~mk[w];
-        if (w > lane && e == NW * 32 && zz) e = w * 32 + __ffs(zz) - 1;
-      }
+    for (int g = 0; g < 32 / RPI; ++g) {
+      const uint32_t grpbits = (m >> (g * RPI)) & ((RPI == 32) ? 0xFFFFFFFFu : ((1u << RPI) - 1u));
+      if (!grpbits) continue;
+      const int r = w * 32 + g * RPI + rsub;
+      if ((grpbits >> rsub) & 1u) cp_async16(dst + r * ROW + chunk * 16, src + r * ROW + chunk * 16);
     }
-    const int r0 = lane * 32 + sb;
-    bulk_g2s(dst + off + r0 * row, src + off + r0 * row, (uint32_t)(e - r0) * row, bar);
   }
 }
 

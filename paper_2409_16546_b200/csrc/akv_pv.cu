@@ -6,10 +6,10 @@
 //                  page's per-head "need mid / need low" row bitmaps written by
 //                  akv_softmax_select (RowMax superset rule; row
 //                  tiers for the row strategy, D7), and streams the page into
-//                  a shared ring with TMA bulk copies: the valid rows of the
-//                  head plane in one copy, only the runs of 64 B mid / low rows
-//                  that some q-head of the kv-head needs, and the per-row
-//                  metadata (p_t, selection bits, need bits, rule-2 targets);
+//                  a shared ring: the valid rows of the head plane in one TMA
+//                  bulk copy; only the 64 B mid / low rows that some q-head of
+//                  the kv-head needs, and the per-row metadata (p_t, selection
+//                  bits, need bits, rule-2 targets), by cp.async from all lanes;
 //  consumer warps  (two groups of four for G <= 2, one group for G >= 4) take
 //                  16 lanes per row x 8 channels per lane, two rows per warp
 //                  instruction.  Rows that no q-head needs beyond T8 take a
@@ -144,25 +144,34 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
   uint8_t* dst = sm.data[stage];
   PvAux<G>& ax = sm.aux[stage];
   const uint32_t vbytes = (uint32_t)rows * D + (uint32_t)(nm + nl) * (D / 2);
-  const uint32_t abytes = (uint32_t)sizeof(PvAux<G>);
   __syncwarp();
   if (lane == 0) {
-    mbar_arrive_expect_tx(&sm.full[stage], vbytes + abytes);
+    // head plane rows: one TMA bulk copy
+    mbar_arrive_expect_tx(&sm.full[stage], (uint32_t)rows * D);
+    bulk_g2s(dst, src, (uint32_t)rows * D, &sm.full[stage]);
     atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)f.u * 4 + 1), (unsigned long long)vbytes);
   }
-  __syncwarp();
-  if (lane == 31) bulk_g2s(dst, src, (uint32_t)rows * D, &sm.full[stage]);
-  if (lane < G) {
-    const size_t h = (size_t)f.u * G + lane;
-    bulk_g2s(ax.probs[lane], st.probs + h * cap + (size_t)f.pg * P, P * 4, &sm.full[stage]);
-    bulk_g2s(ax.targets[lane], st.targets + h * D, D * 4, &sm.full[stage]);
-    bulk_g2s(ax.sel[lane], st.sel_bits + h * (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
-    bulk_g2s(ax.need[lane][0], st.need_bits + h * 2 * (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
-    bulk_g2s(ax.need[lane][1], st.need_bits + h * 2 * (cap >> 5) + (cap >> 5) + f.pg * 8, 32, &sm.full[stage]);
+  // nibble rows (64 B) and per-row metadata: cp.async from all lanes
+  cp_rows<8, D / 2>(um, dst + MID, src + MID);
+  cp_rows<8, D / 2>(ul, dst + LOW, src + LOW);
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const size_t h = (size_t)f.u * G + j;
+    const uint8_t* pr = reinterpret_cast<const uint8_t*>(st.probs + h * cap + (size_t)f.pg * P);
+    cp_async16(reinterpret_cast<uint8_t*>(ax.probs[j]) + lane * 16, pr + lane * 16);
+    cp_async16(reinterpret_cast<uint8_t*>(ax.probs[j]) + 512 + lane * 16, pr + 512 + lane * 16);
+    cp_async16(reinterpret_cast<uint8_t*>(ax.targets[j]) + lane * 16,
+               reinterpret_cast<const uint8_t*>(st.targets + h * D) + lane * 16);
+    if (lane < 2) cp_async16(reinterpret_cast<uint8_t*>(ax.sel[j]) + lane * 16,
+                             reinterpret_cast<const uint8_t*>(st.sel_bits + h * (cap >> 5) + f.pg * 8) + lane * 16);
+    else if (lane < 6) {
+      const int q = lane - 2;  // need[0] chunks 0,1 then need[1] chunks 0,1
+      const uint32_t* nsrc = st.need_bits + h * 2 * (cap >> 5) + (q >> 1) * (cap >> 5) + f.pg * 8;
+      cp_async16(reinterpret_cast<uint8_t*>(ax.need[j][q >> 1]) + (q & 1) * 16,
+                 reinterpret_cast<const uint8_t*>(nsrc) + (q & 1) * 16);
+    }
   }
-  // runs of rows needing the mid / low nibble row
-  bulk_runs<8>(um, dst, src, MID, D / 2, &sm.full[stage]);
-  bulk_runs<8>(ul, dst, src, LOW, D / 2, &sm.full[stage]);
+  cp_async_arrive_noinc(&sm.full[stage]);
 }
 
 // ----------------------------------------------------------------------------
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.full[i], 33);  // expect_tx arrival + 32 cp.async arrivals
       mbar_init(&sm.empty[i], 4);
     }
     mbar_fence_init();
@@ -379,10 +388,10 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
     for (int t = 0; t < NG; ++t, ++k) {
       const int stage = k % NS;
       mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
-      if (lane == 0) {
-        sm.meta[stage].item = -1;
-        mbar_arrive(&sm.full[stage]);
-      }
+      if (lane == 0) sm.meta[stage].item = -1;
+      __syncwarp();
+      mbar_arrive(&sm.full[stage]);  // 32 lane arrivals ...
+      if (lane == 0) mbar_arrive(&sm.full[stage]);  // ... + the expect_tx slot
       __syncwarp();
     }
   } else {

@@ -10,8 +10,10 @@
 //                  tier codes, and streams the page into a 3-stage shared
 //                  ring with TMA bulk copies (cp.async.bulk + mbarrier
 //                  complete_tx): the whole 32 KB head plane in one copy, and
-//                  only the runs of 128 B mid / low channel rows whose union
+//                  only the 128 B mid / low channel rows whose union
 //                  tier needs them (SKIP / T8 channels read 8 bits or nothing);
+//                  (rows fetched by cp.async from all 32 lanes: TMA pays a
+//                  fixed cost per bulk copy, too high for 128 B rows);
 //  2 x 4 consumer  warps (two pages in flight) rebuild the fp16 words from
 //                  shared memory with PRMT/LOP3 (midpoint fill for absent
 //                  nibbles, HB:160-179) and accumulate q_c * K~ with the
@@ -246,18 +248,17 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     mt.n = f.n;
     mt.nlist = nlp;
   }
-  // TMA: head plane in one copy, mid / low rows as runs of consecutive channels
+  // head plane: one 32 KB TMA bulk copy; mid / low channel rows (128 B each): cp.async by all lanes
   const uint8_t* src = page_ptr(s.k_pool, s.page_table, s.max_pages, f.u, f.pg);
   uint8_t* dst = sm.data[stage];
-  const uint32_t bytes = (uint32_t)(D * P) + (uint32_t)(nm + nlo) * (P / 2);
   __syncwarp();
   if (lane == 0) {
-    mbar_arrive_expect_tx(&sm.full[stage], bytes);
+    mbar_arrive_expect_tx(&sm.full[stage], D * P);
     bulk_g2s(dst, src, D * P, &sm.full[stage]);
   }
-  __syncwarp();
-  bulk_runs<4>(bm, dst, src, MID, P / 2, &sm.full[stage]);
-  bulk_runs<4>(bl, dst, src, LOW, P / 2, &sm.full[stage]);
+  cp_rows<4, P / 2>(bm, dst + MID, src + MID);
+  cp_rows<4, P / 2>(bl, dst + LOW, src + LOW);
+  cp_async_arrive_noinc(&sm.full[stage]);
 }
 
 // ----------------------------------------------------------------------------
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < QK_NS; ++i) {
-      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.full[i], 33);  // expect_tx arrival + 32 cp.async arrivals
       mbar_init(&sm.empty[i], 4);
     }
     mbar_fence_init();
@@ -427,10 +428,10 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
     for (int t = 0; t < 2; ++t, ++k) {
       const int stage = k % QK_NS;
       mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
-      if (lane == 0) {
-        sm.meta[stage].item = -1;
-        mbar_arrive(&sm.full[stage]);
-      }
+      if (lane == 0) sm.meta[stage].item = -1;
+      __syncwarp();
+      mbar_arrive(&sm.full[stage]);  // 32 lane arrivals ...
+      if (lane == 0) mbar_arrive(&sm.full[stage]);  // ... + the expect_tx slot
       __syncwarp();
     }
   } else {
