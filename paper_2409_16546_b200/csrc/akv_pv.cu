@@ -208,14 +208,27 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
   uint8_t* vt = (EXPORT && st.v_tiers) ? st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P) * D + cl * 8 : nullptr;
 
   const int r0 = w4 * 64;
+  // pre-pass over this warp's 64 rows: fold selection (D6) and the page end into p (0 -> no contribution)
+  float* pw = const_cast<float*>(&ax.probs[0][0]);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int r = r0 + lane + 32 * k;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const bool drop = r >= rows || (aligned && bit8(ax.sel[j], r));
+      if (drop) pw[j * P + r] = 0.f;
+    }
+  }
+  __syncwarp();
+  const int npairs = min(max((rows - r0 + 1) >> 1, 0), 32);
 #pragma unroll 2
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < npairs; ++i) {
     const int r = r0 + 2 * i + half;
-    if (r >= rows) continue;
-    const uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
-    const bool nm = bit8(mt.un_mid, r);
-    if (aligned && !nm) {
-      // no q-head needs more than the head byte on this row: T8 (or skipped)
+    uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
+    if (r >= rows) h = make_uint2(0u, 0u);  // odd tail row: not copied this page
+    const uint32_t pairbits = (mt.un_mid[(r0 + 2 * i) >> 5] >> ((r0 + 2 * i) & 31)) & 3u;  // warp-uniform
+    if (aligned && !pairbits) {
+      // no q-head needs more than the head byte on these two rows: T8 (or p = 0)
       uint32_t w[4];
       t8_words(h, w);
       float2 f[4];
@@ -223,17 +236,18 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
       for (int k = 0; k < 4; ++k) f[k] = half2_bits_to_float2(w[k]);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const bool sel = bit8(ax.sel[j], r);
-        const float p = sel ? 0.f : ax.probs[j][r];
+        const float p = ax.probs[j][r];
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(f[k], p, acc[j][k]);
-        if (EXPORT && vt) {
-          const uint32_t c = sel ? 0x10101010u : 0x08080808u;
+        if (EXPORT && vt && r < rows) {
+          const uint32_t c = bit8(ax.sel[j], r) ? 0x10101010u : 0x08080808u;
           *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(c, c);
         }
       }
       continue;
     }
+    if (r >= rows) continue;
+    const bool nm = bit8(mt.un_mid, r);
     const uint32_t mv = nm ? *reinterpret_cast<const uint32_t*>(pgd + MID + r * (D / 2) + cl * 4) : 0u;
     const bool nl = bit8(mt.un_low, r);
     const uint32_t lv = nl ? *reinterpret_cast<const uint32_t*>(pgd + LOW + r * (D / 2) + cl * 4) : 0u;

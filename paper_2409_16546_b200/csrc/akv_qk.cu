@@ -73,10 +73,10 @@ __device__ __forceinline__ void fma8(const uint32_t w[4], uint32_t qpair, float 
 template <int G>
 struct alignas(16) QkMeta {
   int item, u, pg, n;
-  int nlist, pad0, pad1, pad2;
-  uint16_t ent[D];          // channel | union class << 8 ; class 0 = pad
-  uint32_t q[G][D / 2];     // q (fp16) per list position, pairs; 0 for SKIP heads / pads
-  uint8_t code[G][D];       // per-head read code per list position (8/12/16; SKIP -> 8 with q = 0)
+  int n8p, nlist, pad1, pad2;  // T8-class range [0, n8p), full range [n8p, nlist); both padded to 8
+  uint16_t ent[D + 8];      // channel | has_low << 8 (pads: channel 0, q = 0)
+  uint32_t q[G][D / 2 + 4]; // q (fp16) per list position, pairs; 0 for SKIP heads / pads
+  uint8_t code[G][D + 8];       // per-head read code per list position (8/12/16; SKIP -> 8 with q = 0)
 };
 
 template <int G>
@@ -210,16 +210,17 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     nm += __popc(bm[k]);
     nlo += __popc(bl[k]);
   }
-  const int nl = n8 + nm, nlp = (nl + 7) & ~7;
+  const int nl = n8 + nm;
+  const int n8p = (n8 + 7) & ~7, nlp = n8p + ((nm + 7) & ~7);
   int base8 = 0, basem = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int c = lane + 32 * k;
     int pos = -1;
     if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
-    else if (ucode[k] >= 12) pos = n8 + basem + __popc(bm[k] & lt);
+    else if (ucode[k] >= 12) pos = n8p + basem + __popc(bm[k] & lt);
     if (pos >= 0) {
-      mt.ent[pos] = (uint16_t)(c | (ucode[k] << 8));
+      mt.ent[pos] = (uint16_t)(c | ((ucode[k] == 16 ? 1 : 0) << 8));
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         reinterpret_cast<uint16_t*>(mt.q[j])[pos] = code[j][k] ? (uint16_t)f.qw[j][k] : (uint16_t)0;
@@ -229,12 +230,24 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     base8 += __popc(b8[k]);
     basem += __popc(bm[k]);
   }
-  for (int pos = nl + lane; pos < nlp; pos += 32) {
-    mt.ent[pos] = 0;
+  // pads (channel 0, q = 0): the head plane is always resident, so the word is finite and adds 0
+  if (lane < 8) {
+    const int p0 = n8 + lane, p1 = n8p + nm + lane;
+    if (p0 < n8p) {
+      mt.ent[p0] = 0;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      reinterpret_cast<uint16_t*>(mt.q[j])[pos] = 0;
-      mt.code[j][pos] = 8;
+      for (int j = 0; j < G; ++j) {
+        reinterpret_cast<uint16_t*>(mt.q[j])[p0] = 0;
+        mt.code[j][p0] = 8;
+      }
+    }
+    if (p1 < nlp) {
+      mt.ent[p1] = 0;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        reinterpret_cast<uint16_t*>(mt.q[j])[p1] = 0;
+        mt.code[j][p1] = 8;
+      }
     }
   }
   if (book && lane == 0) {
@@ -246,6 +259,7 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     mt.u = f.u;
     mt.pg = f.pg;
     mt.n = f.n;
+    mt.n8p = n8p;
     mt.nlist = nlp;
   }
   // head plane: one 32 KB TMA bulk copy; mid / low channel rows (128 B each): cp.async by all lanes
@@ -273,7 +287,7 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
   const uint8_t* pgd = sm.data[stage];
   const int cs = w4 % CS;
   const int j0 = (w4 / CS) * HW;  // first head of this warp
-  const int nb = mt.nlist >> 3;
+  const int nb8 = mt.n8p >> 3, nb = mt.nlist >> 3;
   const int u = mt.u, pg = mt.pg, n = mt.n;  // read before the stage is released
   float acc[HW][8];
 #pragma unroll
@@ -283,27 +297,45 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
   const uint8_t* hb = pgd + lane * 8;
   const uint8_t* mb = pgd + MID + lane * 4;
 
-  for (int b = cs; b < nb; b += CS) {
+  // T8-class channels: head byte only (all q-heads read T8 or SKIP with q = 0)
+  for (int b = cs; b < nb8; b += CS) {
+    const uint4 e4 = *reinterpret_cast<const uint4*>(&mt.ent[b * 8]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t ch = ent_of(e4, i) & 0xFFu;
+      const uint2 h = *reinterpret_cast<const uint2*>(hb + ch * P);
+      const uint32_t c80 = 0x80808080u;
+      uint32_t w[4];
+      w[0] = prmt(h.x, c80, 0x1404);
+      w[1] = prmt(h.x, c80, 0x3424);
+      w[2] = prmt(h.y, c80, 0x1404);
+      w[3] = prmt(h.y, c80, 0x3424);
+      if (TRUNC) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
+      }
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj) {
+        const uint32_t qp = mt.q[j0 + jj][b * 4 + (i >> 1)];
+        if (i & 1) fma8<1>(w, qp, acc[jj]);
+        else fma8<0>(w, qp, acc[jj]);
+      }
+    }
+  }
+  // T12/T16-class channels: head + mid (+ low) rows
+  const int bf0 = nb8 + ((cs - nb8 % CS) % CS + CS) % CS;
+  for (int b = bf0; b < nb; b += CS) {
     const uint4 e4 = *reinterpret_cast<const uint4*>(&mt.ent[b * 8]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t en = ent_of(e4, i);
-      const uint32_t ch = en & 0xFFu, cls = en >> 8;
-      if (cls == 0) continue;  // pad (warp-uniform)
-      const int pos = b * 8 + i;
+      const uint32_t ch = en & 0xFFu;
       const uint2 h = *reinterpret_cast<const uint2*>(hb + ch * P);
+      const uint32_t m = *reinterpret_cast<const uint32_t*>(mb + ch * (P / 2));
+      uint32_t l = 0x88888888u;
+      if (en >> 8) l = *reinterpret_cast<const uint32_t*>(mb + (LOW - MID) + ch * (P / 2));
       uint32_t w[4];
-      if (cls == 8) {
-        const uint32_t c80 = 0x80808080u;
-        w[0] = prmt(h.x, c80, 0x1404);
-        w[1] = prmt(h.x, c80, 0x3424);
-        w[2] = prmt(h.y, c80, 0x1404);
-        w[3] = prmt(h.y, c80, 0x3424);
-      } else {
-        const uint32_t m = *reinterpret_cast<const uint32_t*>(mb + ch * (P / 2));
-        const uint32_t l = cls == 16 ? *reinterpret_cast<const uint32_t*>(mb + (LOW - MID) + ch * (P / 2)) : 0x88888888u;
-        assemble8(h.x, h.y, m, l, w);
-      }
+      assemble8(h.x, h.y, m, l, w);
       if (TRUNC) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) w[k] = (w[k] & tkm) | tf;
@@ -312,8 +344,8 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
       for (int jj = 0; jj < HW; ++jj) {
         const int j = j0 + jj;
         uint32_t wj[4];
-        if (G > 1 && cls != 8) {
-          const uint32_t cd = mt.code[j][pos];
+        if (G > 1) {
+          const uint32_t cd = mt.code[j][b * 8 + i];
           const uint32_t km = cd >= 16 ? 0xFFFFFFFFu : (cd == 12 ? 0xFFF0FFF0u : 0xFF00FF00u);
           const uint32_t fl = cd >= 16 ? 0u : (cd == 12 ? 0x00080008u : 0x00800080u);
 #pragma unroll
@@ -322,7 +354,7 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
 #pragma unroll
           for (int k = 0; k < 4; ++k) wj[k] = w[k];
         }
-        const uint32_t qp = mt.q[j][pos >> 1];
+        const uint32_t qp = mt.q[j][b * 4 + (i >> 1)];
         if (i & 1) fma8<1>(wj, qp, acc[jj]);
         else fma8<0>(wj, qp, acc[jj]);
       }
