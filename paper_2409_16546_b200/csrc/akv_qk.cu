@@ -2,11 +2,11 @@
 //
 // Warp-specialised persistent kernel, one CTA per SM:
 //
-//  producer warp   walks a static strided (unit, page) schedule (its loads
-//                  are issued one item ahead), evaluates Rule 1 for the unit's q-heads
+//  producer warp   walks a contiguous range of (unit, page) items, evaluates Rule 1 for the unit's q-heads
 //                  (rule1_target SPEC.md:157-165, required_mantissa_bits
 //                  :139-147, tier_for_bits :148-156, k_channel_tiers :175-183,
-//                  SURVEY App. A A-K/D1/D2/D8), publishes the channel list and
+//                  SURVEY App. A A-K/D1/D2/D8) once per unit (the next unit's q and
+//                  ColMax are prefetched), publishes the channel list and
 //                  tier codes, and streams the page into a 3-stage shared
 //                  ring with TMA bulk copies (cp.async.bulk + mbarrier
 //                  complete_tx): the whole 32 KB head plane in one copy, and
@@ -83,6 +83,7 @@ template <int G>
 struct alignas(128) QkSmem {
   uint8_t data[QK_NS][PAGE];
   QkMeta<G> meta[QK_NS];
+  QkMeta<G> cache;           // producer-private: the current unit's list (copied into each stage)
   float red[2][4][P];        // partial token sums per group / warp (channel split, G <= 2)
   float stat[2][4][2];
   uint64_t full[QK_NS], empty[QK_NS];
@@ -103,25 +104,17 @@ __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
 // producer
 // ----------------------------------------------------------------------------
 template <int G>
-struct QkPrefetch {
-  int item, u, pg, n;
+struct QkUnit {
+  int u, n;
   uint32_t cm[4];
   uint32_t qw[G][4];
 };
 
-// Issue the loads an item needs (no wait: the registers are consumed one item later).
+// Issue the loads a unit's Rule-1 prologue needs (no wait: consumed later).
 template <int G>
-__device__ __forceinline__ void qk_fetch(QkPrefetch<G>& f, const akv_store_t& s, const akv_step_t& st, int npg_max,
-                                         long long idx, long long total) {
+__device__ __forceinline__ void qk_fetch_unit(QkUnit<G>& f, const akv_store_t& s, const akv_step_t& st, int u) {
   const int lane = threadIdx.x & 31;
-  if (idx >= total) {
-    f.item = -1;
-    return;
-  }
-  const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
-  f.item = (int)idx;
   f.u = u;
-  f.pg = pg;
   f.n = s.lengths[u];
 #pragma unroll
   for (int k = 0; k < 4; ++k) f.cm[k] = s.colmax[(size_t)u * D + lane + 32 * k];
@@ -131,13 +124,15 @@ __device__ __forceinline__ void qk_fetch(QkPrefetch<G>& f, const akv_store_t& s,
     for (int k = 0; k < 4; ++k) f.qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
 }
 
+// Rule 1 for one unit (all q-heads): tier codes, the channel list and the
+// fetch masks; once per unit per CTA.  `book`: this CTA owns the unit's page 0
+// and writes the per-step bookkeeping (K tiers, K counters, status, bytes).
 template <int G, bool TRUNC>
-__device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, const akv_store_t& s,
-                           const akv_cfg_t& cfg, const akv_step_t& st) {
+__device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, const akv_cfg_t& cfg,
+                                 const akv_step_t& st, uint32_t (&bm)[4], uint32_t (&bl)[4]) {
   const int lane = threadIdx.x & 31;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
-  const bool book = f.pg == 0;
-  QkMeta<G>& mt = sm.meta[stage];
+  QkMeta<G>& mt = sm.cache;
   int code[G][4], ucode[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -199,7 +194,7 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
   }
   // channel list (T8 class first, then T12/T16; ascending channel inside a class)
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t b8[4], bm[4], bl[4];
+  uint32_t b8[4];
   int n8 = 0, nm = 0, nlo = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -254,16 +249,33 @@ __device__ void qk_produce(QkSmem<G>& sm, const QkPrefetch<G>& f, int stage, con
     st.unit_bytes[(size_t)f.u * 4 + 0] = (int64_t)f.n * nl + (int64_t)(f.n / 2) * (nm + nlo);
     st.unit_bytes[(size_t)f.u * 4 + 1] = 0;
   }
+  (void)nl;
   if (lane == 0) {
-    mt.item = f.item;
-    mt.u = f.u;
-    mt.pg = f.pg;
-    mt.n = f.n;
     mt.n8p = n8p;
     mt.nlist = nlp;
   }
-  // head plane: one 32 KB TMA bulk copy; mid / low channel rows (128 B each): cp.async by all lanes
-  const uint8_t* src = page_ptr(s.k_pool, s.page_table, s.max_pages, f.u, f.pg);
+  __syncwarp();
+}
+
+// Publish one page into a ring stage: the cached unit list + item fields, then
+// the copies (head plane by TMA bulk copy; needed mid / low rows by cp.async).
+template <int G>
+__device__ void qk_stage(QkSmem<G>& sm, int stage, int item, int u, int pg, int n, const akv_store_t& s,
+                         const uint32_t (&bm)[4], const uint32_t (&bl)[4]) {
+  const int lane = threadIdx.x & 31;
+  QkMeta<G>& mt = sm.meta[stage];
+  constexpr int W = sizeof(QkMeta<G>) / 16;
+  const uint4* srcm = reinterpret_cast<const uint4*>(&sm.cache);
+  uint4* dstm = reinterpret_cast<uint4*>(&mt);
+  for (int i = lane; i < W; i += 32) dstm[i] = srcm[i];
+  __syncwarp();
+  if (lane == 0) {
+    mt.item = item;
+    mt.u = u;
+    mt.pg = pg;
+    mt.n = n;
+  }
+  const uint8_t* src = page_ptr(s.k_pool, s.page_table, s.max_pages, u, pg);
   uint8_t* dst = sm.data[stage];
   __syncwarp();
   if (lane == 0) {
@@ -440,20 +452,26 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
   const long long total = (long long)s.n_units * npg_max;
 
   if (warp == 0) {
-    // ---------------- producer: static strided item schedule, loads one item ahead ----------------
-    QkPrefetch<G> cur, nxt;
-    long long idx = blockIdx.x;
-    qk_fetch<G>(nxt, s, st, npg_max, idx, total);
+    // ---------------- producer: contiguous item range, Rule 1 once per unit ----------------
+    const long long per = (total + gridDim.x - 1) / gridDim.x;
+    const long long i0 = (long long)blockIdx.x * per, i1 = min(total, i0 + per);
+    QkUnit<G> cur, nxt;
+    uint32_t bm[4] = {0, 0, 0, 0}, bl[4] = {0, 0, 0, 0};
+    int cur_u = -1;
+    if (i0 < i1) qk_fetch_unit<G>(nxt, s, st, (int)(i0 / npg_max));
     int k = 0;
-    for (;;) {
-      cur = nxt;
-      if (cur.item < 0) break;
-      idx += gridDim.x;
-      qk_fetch<G>(nxt, s, st, npg_max, idx, total);
-      if (cur.pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
+    for (long long idx = i0; idx < i1; ++idx) {
+      const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
+      if (u != cur_u) {
+        cur = nxt;
+        if ((long long)(u + 1) * npg_max < i1) qk_fetch_unit<G>(nxt, s, st, u + 1);  // prefetch the next unit
+        cur_u = u;
+        if (cur.n > 0) qk_unit_prologue<G, TRUNC>(sm, cur, pg == 0, cfg, st, bm, bl);
+      }
+      if (pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
       const int stage = k % QK_NS;
       mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
-      qk_produce<G, TRUNC>(sm, cur, stage, s, cfg, st);
+      qk_stage<G>(sm, stage, (int)idx, u, pg, cur.n, s, bm, bl);
       ++k;
     }
     // one terminator per consumer group

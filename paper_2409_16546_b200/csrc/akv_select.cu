@@ -79,26 +79,36 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
   float* pr = st.probs + (size_t)h * cap;
   uint32_t* bits = st.sel_bits + (size_t)h * (cap >> 5);
 
-  // 2. probabilities, bitmap reset, candidate compaction
-  for (int t0 = 0; t0 < n; t0 += ST) {
-    const int t = t0 + tid;
-    bool cand = false;
-    float p = 0.f;
-    if (t < n) {
-      p = expf(sc[t] - M) / L;
-      pr[t] = p;
-      cand = est && p >= thr;
+  // 2. probabilities, bitmap reset, candidate compaction (loads batched BT deep)
+  constexpr int BT = 8;
+  for (int t0 = 0; t0 < n; t0 += ST * BT) {
+    float sv[BT];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int t = t0 + b * ST + tid;
+      sv[b] = t < n ? sc[t] : 0.f;
     }
-    if (lane == 0 && t < n) bits[t >> 5] = 0u;
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, cand);
-    if (b) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&sm.ncand, __popc(b));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      const int slot = base + __popc(b & ((1u << lane) - 1u));
-      if (cand && slot < CAND) {
-        sm.cand_t[slot] = t;
-        sm.cand_p[slot] = p;
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int t = t0 + b * ST + tid;
+      bool cand = false;
+      float p = 0.f;
+      if (t < n) {
+        p = expf(sv[b] - M) / L;
+        pr[t] = p;
+        cand = est && p >= thr;
+      }
+      if (lane == 0 && t < n) bits[t >> 5] = 0u;
+      const unsigned bb = __ballot_sync(0xFFFFFFFFu, cand);
+      if (bb) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&sm.ncand, __popc(bb));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        const int slot = base + __popc(bb & ((1u << lane) - 1u));
+        if (cand && slot < CAND) {
+          sm.cand_t[slot] = t;
+          sm.cand_p[slot] = p;
+        }
       }
     }
   }
@@ -244,38 +254,51 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
   //    element strategy: RowMax superset bound (H6); row strategy: the row tier (D7)
   {
     uint32_t* nb = st.need_bits + (size_t)h * 2 * (cap >> 5);
-    for (int t0 = 0; t0 < n; t0 += ST) {
-      const int t = t0 + tid;
-      bool nm = false, nlw = false;
-      if (t < n && est) {
-        const bool sel = (bits[t >> 5] >> (t & 31)) & 1u;
-        const float p = pr[t];
-        const uint32_t rm = s.rowmax[(size_t)u * s.max_pages * P + t];
-        if (!sel && cfg.strategy == 1) {
-          int tier = 16;
-          if (!unk_all) {
-            if (p == 0.f || rm == 0) tier = 8;
-            else {
-              const int tr = min(max(floor_log2f(p) + magexp16(rm) + 1 - tmin_all - 1 + cfg.margin_bits, 0), 10);
-              tier = tr <= 2 ? 8 : (tr <= 6 ? 12 : 16);
+    for (int t0 = 0; t0 < n; t0 += ST * BT) {
+      float pv[BT];
+      uint32_t rmv[BT], selw[BT];
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        const int t = t0 + b * ST + tid;
+        const bool in = t < n && est;
+        pv[b] = in ? pr[t] : 0.f;
+        rmv[b] = in ? (uint32_t)s.rowmax[(size_t)u * s.max_pages * P + t] : 0u;
+        selw[b] = in ? bits[t >> 5] : 0u;
+      }
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        const int t = t0 + b * ST + tid;
+        bool nm = false, nlw = false;
+        if (t < n && est) {
+          const bool sel = (selw[b] >> (t & 31)) & 1u;
+          const float p = pv[b];
+          const uint32_t rm = rmv[b];
+          if (!sel && cfg.strategy == 1) {
+            int tier = 16;
+            if (!unk_all) {
+              if (p == 0.f || rm == 0) tier = 8;
+              else {
+                const int tr = min(max(floor_log2f(p) + magexp16(rm) + 1 - tmin_all - 1 + cfg.margin_bits, 0), 10);
+                tier = tr <= 2 ? 8 : (tr <= 6 ? 12 : 16);
+              }
+            }
+            nm = tier >= 12;
+            nlw = tier == 16;
+          } else if (!sel && p > 0.f) {
+            if (unk_all) {
+              nm = nlw = true;
+            } else {
+              const int bound = floor_log2f(p) + (max(bexp16(rm), 1) - 15) + 1 - tmin_all - 1 + cfg.margin_bits;
+              nm = bound > 2;
+              nlw = bound > 6;
             }
           }
-          nm = tier >= 12;
-          nlw = tier == 16;
-        } else if (!sel && p > 0.f) {
-          if (unk_all) {
-            nm = nlw = true;
-          } else {
-            const int bound = floor_log2f(p) + (max(bexp16(rm), 1) - 15) + 1 - tmin_all - 1 + cfg.margin_bits;
-            nm = bound > 2;
-            nlw = bound > 6;
-          }
         }
-      }
-      const unsigned bm = __ballot_sync(0xFFFFFFFFu, nm), bl = __ballot_sync(0xFFFFFFFFu, nlw);
-      if (lane == 0 && t < n) {
-        nb[t >> 5] = bm;
-        nb[(cap >> 5) + (t >> 5)] = bl;
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, nm), bl = __ballot_sync(0xFFFFFFFFu, nlw);
+        if (lane == 0 && t < n) {
+          nb[t >> 5] = bm;
+          nb[(cap >> 5) + (t >> 5)] = bl;
+        }
       }
     }
   }
