@@ -1,27 +1,31 @@
 // output_aligned for every (unit, q-head).
 //
-// Warp-specialised persistent kernel, one CTA per SM:
+// Warp-specialised persistent kernel, one CTA per SM, 6-stage shared ring of
+// half pages (128 V rows: 16 KB head rows + up to 8 KB mid + 8 KB low rows +
+// the rows' metadata), two half-page stages per page:
 //
-//  producer warp   walks a static strided (unit, page) schedule, reads the
+//  producer warp   walks a contiguous range of (unit, page) items, reads the
 //                  page's per-head "need mid / need low" row bitmaps written by
 //                  akv_softmax_select (RowMax superset rule; row
-//                  tiers for the row strategy, D7), and streams the page into
-//                  a shared ring: the valid rows of the head plane in one TMA
-//                  bulk copy; only the 64 B mid / low rows that some q-head of
-//                  the kv-head needs, and the per-row metadata (p_t, selection
-//                  bits, need bits, rule-2 targets), by cp.async from all lanes;
-//  consumer warps  (two groups of four for G <= 2, one group for G >= 4) take
+//                  tiers for the row strategy, D7) one page ahead, and fills
+//                  each stage: the head rows by one TMA bulk copy; only the
+//                  64 B mid / low rows some q-head of the kv-head needs, and
+//                  the per-row metadata (p_t, selection bits, need bits,
+//                  rule-2 targets), by cp.async from all 32 lanes;
+//  consumer warps  (two groups of four for G <= 2, one group for G >= 4):
 //                  16 lanes per row x 8 channels per lane, two rows per warp
-//                  instruction.  Rows that no q-head needs beyond T8 take a
-//                  branch-free path (4 PRMT per 8 elements); otherwise each
-//                  head applies its own rule: selected rows are skipped (D6:
-//                  their T16 contribution is already in o_est), p_t = 0 rows
-//                  read T8 (D5), ELEMENT rows keep mid iff
-//                  max(bexp,1) + e(p_t) > 17 + target_r - margin and low iff
-//                  > that + 4 (D4), row-strategy rows use the row tier (D7).
-//                  Truncation is applied after the fetch, so the masks are the
-//                  oracle's bit for bit.  fp16 -> fp32 by HADD2.F32 and
-//                  p_t * V~ by the packed FFMA2 into fp32.
+//                  instruction, 32 rows per warp per half page.  A per-half
+//                  pre-pass folds the selection (D6: selected rows' T16
+//                  contribution is already in o_est) and the page end into p.
+//                  A 32-row block that no q-head needs beyond T8 takes a
+//                  branch-free unrolled path (4 PRMT per 8 elements); other
+//                  rows apply each head's rule: p_t = 0 -> T8 (D5); ELEMENT:
+//                  keep mid iff max(bexp,1) + e(p_t) > 17 + target_r - margin,
+//                  low iff > that + 4 (D4); row strategy: the row tier (D7);
+//                  forced / baseline tiers.  Truncation is applied after the
+//                  fetch, so the masks equal the oracle's bit for bit.  fp16 ->
+//                  fp32 by HADD2.F32 and p_t * V~ by the packed FFMA2 into fp32
+//                  (SPEC.md:379).
 // The page's partial output goes to o_partial[h][page]; akv_combine adds o_est
 // and the partials in a fixed order (deterministic).
 #include <algorithm>
@@ -30,36 +34,41 @@
 
 namespace akv {
 
+constexpr int HR = P / 2;                // rows per half page
+constexpr int VS = HR * D * 2;           // 32 KB: head [128][128] | mid [128][64] | low [128][64]
+constexpr int VS_MID = HR * D, VS_LOW = HR * D + HR * (D / 2);
+
 template <int G>
 struct PvShape {
-  static constexpr int NG = G >= 4 ? 1 : 2;       // consumer groups (pages in flight)
-  static constexpr int NS = G >= 4 ? 2 : 3;       // ring stages
+  static constexpr int NG = G >= 4 ? 1 : 2;  // consumer groups (pages in flight)
+  static constexpr int NS = G >= 8 ? 4 : 6;  // ring stages (half pages)
   static constexpr int THREADS = 32 * (1 + 4 * NG);
 };
 
 template <int G>
-struct alignas(16) PvAux {   // TMA-copied per-row / per-head metadata of one page
-  float probs[G][P];
+struct alignas(16) PvAux {  // per-row / per-head metadata of one half page (cp.async)
+  float probs[G][HR];
   int32_t targets[G][D];
-  uint32_t sel[G][8];
-  uint32_t need[G][2][8];
+  uint32_t sel[G][4];
+  uint32_t need[G][2][4];
 };
 
 struct alignas(16) PvMeta {
   int item, u, pg, n;
-  uint32_t un_mid[8], un_low[8];  // union over q-heads of the need bitmaps (rows of this page)
+  int half, rows, pad0, pad1;     // rows valid in this half
+  uint32_t un_mid[4], un_low[4];  // union over q-heads of the need bitmaps of this half
 };
 
 template <int G>
 struct alignas(128) PvSmem {
-  uint8_t data[PvShape<G>::NS][PAGE];
+  uint8_t data[PvShape<G>::NS][VS];
   PvAux<G> aux[PvShape<G>::NS];
   PvMeta meta[PvShape<G>::NS];
   float red[PvShape<G>::NG][4][G][D];
   uint64_t full[PvShape<G>::NS], empty[PvShape<G>::NS];
 };
 
-__device__ __forceinline__ bool bit8(const uint32_t* w, int r) { return (w[r >> 5] >> (r & 31)) & 1u; }
+__device__ __forceinline__ bool bitw(const uint32_t* w, int r) { return (w[r >> 5] >> (r & 31)) & 1u; }
 
 __device__ __forceinline__ void t8_words(uint2 h, uint32_t w[4]) {
   const uint32_t c80 = 0x80808080u;
@@ -72,26 +81,17 @@ __device__ __forceinline__ void t8_words(uint2 h, uint32_t w[4]) {
 // ----------------------------------------------------------------------------
 // producer
 // ----------------------------------------------------------------------------
-struct PvPrefetch {
-  int item, u, pg, n;
-  uint32_t um, ul;  // lane w < 8: union need words w of this page
+struct PvPage {
+  int u, n;
+  uint32_t um, ul;  // lane w < 8: union need words w of the page
 };
 
-// Issue the loads an item needs (no wait: the registers are consumed one item later).
 template <int G>
-__device__ __forceinline__ void pv_fetch(PvPrefetch& f, const akv_store_t& s, const akv_cfg_t& cfg,
-                                         const akv_step_t& st, int npg_max, long long idx, long long total, int cap,
-                                         bool uniform) {
+__device__ __forceinline__ void pv_fetch(PvPage& f, const akv_cfg_t& cfg, const akv_step_t& st, int u, int pg,
+                                         int n, int cap, bool uniform) {
   const int lane = threadIdx.x & 31;
-  if (idx >= total) {
-    f.item = -1;
-    return;
-  }
-  const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
-  f.item = (int)idx;
   f.u = u;
-  f.pg = pg;
-  f.n = s.lengths[u];
+  f.n = n;
   f.um = f.ul = 0u;
   if (lane < 8) {
     if (uniform) {
@@ -109,67 +109,74 @@ __device__ __forceinline__ void pv_fetch(PvPrefetch& f, const akv_store_t& s, co
 }
 
 template <int G>
-__device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const akv_store_t& s,
-                           const akv_step_t& st, int cap) {
+__device__ void pv_stage(PvSmem<G>& sm, int stage, int hf, int item, int pg, const PvPage& f, const akv_store_t& s,
+                         const akv_step_t& st, int cap) {
   const int lane = threadIdx.x & 31;
   PvMeta& mt = sm.meta[stage];
-  uint32_t um[8], ul[8];
-  // rows beyond n hold stale bits
-  const int vlo = (lane & 7) * 32, valid = min(max(f.n - f.pg * P - vlo, 0), 32);
-  const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-  const uint32_t m0 = f.um & vm, l0 = f.ul & vm;
+  const int rows = min(max(f.n - pg * P - hf * HR, 0), HR);
+  // this half's need words (rows beyond n hold stale bits)
+  uint32_t um[4], ul[4];
+  {
+    const int lo = (lane & 7) * 32, valid = min(max(f.n - pg * P - lo, 0), 32);
+    const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+    const uint32_t m0 = f.um & vm, l0 = f.ul & vm;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    um[w] = __shfl_sync(0xFFFFFFFFu, m0, w);
-    ul[w] = __shfl_sync(0xFFFFFFFFu, l0, w);
+    for (int w = 0; w < 4; ++w) {
+      um[w] = __shfl_sync(0xFFFFFFFFu, m0, 4 * hf + w);
+      ul[w] = __shfl_sync(0xFFFFFFFFu, l0, 4 * hf + w);
+    }
   }
   int nm = 0, nl = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < 4; ++w) {
     nm += __popc(um[w]);
     nl += __popc(ul[w]);
   }
-  const int rows = min(f.n - f.pg * P, P);
   if (lane == 0) {
-    mt.item = f.item;
+    mt.item = item;
     mt.u = f.u;
-    mt.pg = f.pg;
+    mt.pg = pg;
     mt.n = f.n;
+    mt.half = hf;
+    mt.rows = rows;
   }
-  if (lane < 8) {
-    mt.un_mid[lane] = m0;
-    mt.un_low[lane] = l0;
+  if (lane < 4) {
+    uint32_t a = um[0], b = ul[0];
+#pragma unroll
+    for (int w = 1; w < 4; ++w)
+      if (lane == w) {
+        a = um[w];
+        b = ul[w];
+      }
+    mt.un_mid[lane] = a;
+    mt.un_low[lane] = b;
   }
-  const uint8_t* src = page_ptr(s.v_pool, s.page_table, s.max_pages, f.u, f.pg);
+  const uint8_t* src = page_ptr(s.v_pool, s.page_table, s.max_pages, f.u, pg);
   uint8_t* dst = sm.data[stage];
   PvAux<G>& ax = sm.aux[stage];
-  const uint32_t vbytes = (uint32_t)rows * D + (uint32_t)(nm + nl) * (D / 2);
   __syncwarp();
   if (lane == 0) {
-    // head plane rows: one TMA bulk copy
+    // head rows of this half: one TMA bulk copy
     mbar_arrive_expect_tx(&sm.full[stage], (uint32_t)rows * D);
-    bulk_g2s(dst, src, (uint32_t)rows * D, &sm.full[stage]);
+    if (rows) bulk_g2s(dst, src + hf * HR * D, (uint32_t)rows * D, &sm.full[stage]);
+    const uint32_t vbytes = (uint32_t)rows * D + (uint32_t)(nm + nl) * (D / 2);
     atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)f.u * 4 + 1), (unsigned long long)vbytes);
   }
   // nibble rows (64 B) and per-row metadata: cp.async from all lanes
-  cp_rows<8, D / 2>(um, dst + MID, src + MID);
-  cp_rows<8, D / 2>(ul, dst + LOW, src + LOW);
+  cp_rows<4, D / 2>(um, dst + VS_MID, src + MID + hf * HR * (D / 2));
+  cp_rows<4, D / 2>(ul, dst + VS_LOW, src + LOW + hf * HR * (D / 2));
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     const size_t h = (size_t)f.u * G + j;
-    const uint8_t* pr = reinterpret_cast<const uint8_t*>(st.probs + h * cap + (size_t)f.pg * P);
+    const uint8_t* pr = reinterpret_cast<const uint8_t*>(st.probs + h * cap + (size_t)pg * P + hf * HR);
     cp_async16(reinterpret_cast<uint8_t*>(ax.probs[j]) + lane * 16, pr + lane * 16);
-    cp_async16(reinterpret_cast<uint8_t*>(ax.probs[j]) + 512 + lane * 16, pr + 512 + lane * 16);
     cp_async16(reinterpret_cast<uint8_t*>(ax.targets[j]) + lane * 16,
                reinterpret_cast<const uint8_t*>(st.targets + h * D) + lane * 16);
-    if (lane < 2) cp_async16(reinterpret_cast<uint8_t*>(ax.sel[j]) + lane * 16,
-                             reinterpret_cast<const uint8_t*>(st.sel_bits + h * (cap >> 5) + f.pg * 8) + lane * 16);
-    else if (lane < 6) {
-      const int q = lane - 2;  // need[0] chunks 0,1 then need[1] chunks 0,1
-      const uint32_t* nsrc = st.need_bits + h * 2 * (cap >> 5) + (q >> 1) * (cap >> 5) + f.pg * 8;
-      cp_async16(reinterpret_cast<uint8_t*>(ax.need[j][q >> 1]) + (q & 1) * 16,
-                 reinterpret_cast<const uint8_t*>(nsrc) + (q & 1) * 16);
-    }
+    const uint32_t* selp = st.sel_bits + h * (cap >> 5) + pg * 8 + hf * 4;
+    const uint32_t* nbp = st.need_bits + h * 2 * (cap >> 5) + pg * 8 + hf * 4;
+    if (lane == 0) cp_async16(ax.sel[j], selp);
+    else if (lane == 1) cp_async16(ax.need[j][0], nbp);
+    else if (lane == 2) cp_async16(ax.need[j][1], nbp + (cap >> 5));
   }
   cp_async_arrive_noinc(&sm.full[stage]);
 }
@@ -178,15 +185,15 @@ __device__ void pv_produce(PvSmem<G>& sm, const PvPrefetch& f, int stage, const 
 // consumer
 // ----------------------------------------------------------------------------
 template <int G, bool TRUNC, bool EXPORT>
-__device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, int w4, const akv_cfg_t& cfg,
-                                           const akv_step_t& st, int cap) {
+__device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4, const akv_cfg_t& cfg,
+                                                const akv_step_t& st, int cap, float2 (&acc)[G][4],
+                                                int (&adj)[G][3]) {
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, cl = lane & 15;
   const PvMeta& mt = sm.meta[stage];
-  const PvAux<G>& ax = sm.aux[stage];
+  PvAux<G>& ax = sm.aux[stage];
   const uint8_t* pgd = sm.data[stage];
-  const int u = mt.u, pg = mt.pg, n = mt.n;
-  const int rows = min(n - pg * P, P);
+  const int u = mt.u, pg = mt.pg, hf = mt.half, rows = mt.rows;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
   const int uni = TRUNC ? 16 : cfg.force_tier;
   uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
@@ -197,38 +204,47 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
     tkm = km | (km << 16);
     tf = fill | (fill << 16);
   }
-  float2 acc[G][4];
-  int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8"
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    adj[j][0] = adj[j][1] = adj[j][2] = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[j][k] = make_float2(0.f, 0.f);
-  }
-  uint8_t* vt = (EXPORT && st.v_tiers) ? st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P) * D + cl * 8 : nullptr;
+  uint8_t* vt = (EXPORT && st.v_tiers)
+                    ? st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P + (size_t)hf * HR) * D + cl * 8
+                    : nullptr;
+  const int r0 = w4 * 32;  // this warp's 32 rows inside the half
 
-  const int r0 = w4 * 64;
-  // pre-pass over this warp's 64 rows: fold selection (D6) and the page end into p (0 -> no contribution)
-  float* pw = const_cast<float*>(&ax.probs[0][0]);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int r = r0 + lane + 32 * k;
+  // base counts: every valid unselected row at T8 (aligned) or at the uniform tier
+  if (w4 == 0 && lane < G) {
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const bool drop = r >= rows || (aligned && bit8(ax.sel[j], r));
-      if (drop) pw[j * P + r] = 0.f;
+      if (j != lane) continue;
+      int nsel = 0;
+      if (aligned) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int valid = min(max(rows - w * 32, 0), 32);
+          const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+          nsel += __popc(ax.sel[j][w] & vm);
+        }
+      }
+      const int base = (rows - nsel) * D;
+      if (aligned || uni == 8) adj[j][0] += base;
+      else if (uni == 12) adj[j][1] += base;
+      else adj[j][2] += base;
     }
   }
-  __syncwarp();
-  const int npairs = min(max((rows - r0 + 1) >> 1, 0), 32);
-#pragma unroll 2
-  for (int i = 0; i < npairs; ++i) {
-    const int r = r0 + 2 * i + half;
-    uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
-    if (r >= rows) h = make_uint2(0u, 0u);  // odd tail row: not copied this page
-    const uint32_t pairbits = (mt.un_mid[(r0 + 2 * i) >> 5] >> ((r0 + 2 * i) & 31)) & 3u;  // warp-uniform
-    if (aligned && !pairbits) {
-      // no q-head needs more than the head byte on these two rows: T8 (or p = 0)
+  if (r0 >= rows) return;
+  // pre-pass: fold the selection (D6) and the page end into p (0 -> no contribution)
+  {
+    const int r = r0 + lane;
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      if (r >= rows || (aligned && bitw(ax.sel[j], r))) ax.probs[j][r] = 0.f;
+    __syncwarp();
+  }
+  const bool full_blk = r0 + 32 <= rows;
+  if (aligned && full_blk && mt.un_mid[w4] == 0) {
+    // fast block: every row is T8 (or p = 0) for every q-head
+    const uint8_t* hp = pgd + (r0 + half) * D + cl * 8;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint2 h = *reinterpret_cast<const uint2*>(hp + i * 2 * D);
       uint32_t w[4];
       t8_words(h, w);
       float2 f[4];
@@ -236,42 +252,52 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
       for (int k = 0; k < 4; ++k) f[k] = half2_bits_to_float2(w[k]);
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const float p = ax.probs[j][r];
+        const float p = ax.probs[j][r0 + 2 * i + half];
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[j][k] = ffma2_scalar(f[k], p, acc[j][k]);
-        if (EXPORT && vt && r < rows) {
-          const uint32_t c = bit8(ax.sel[j], r) ? 0x10101010u : 0x08080808u;
+        if (EXPORT && vt) {
+          const int r = r0 + 2 * i + half;
+          const uint32_t c = bitw(ax.sel[j], r) ? 0x10101010u : 0x08080808u;
           *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(c, c);
         }
       }
-      continue;
     }
+    return;
+  }
+  // generic rows
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + 2 * i + half;
     if (r >= rows) continue;
-    const bool nm = bit8(mt.un_mid, r);
-    const uint32_t mv = nm ? *reinterpret_cast<const uint32_t*>(pgd + MID + r * (D / 2) + cl * 4) : 0u;
-    const bool nl = bit8(mt.un_low, r);
-    const uint32_t lv = nl ? *reinterpret_cast<const uint32_t*>(pgd + LOW + r * (D / 2) + cl * 4) : 0u;
+    const uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
+    const bool nm = bitw(mt.un_mid, r), nl = bitw(mt.un_low, r);
+    const uint32_t mv = nm ? *reinterpret_cast<const uint32_t*>(pgd + VS_MID + r * (D / 2) + cl * 4) : 0u;
+    const uint32_t lv = nl ? *reinterpret_cast<const uint32_t*>(pgd + VS_LOW + r * (D / 2) + cl * 4) : 0u;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const float p = ax.probs[j][r];
       int mode;  // 0 skip, 1 element, 8/12/16 uniform tier
       if (!aligned) mode = uni;
-      else if (bit8(ax.sel[j], r)) mode = 0;
-      else if (!bit8(ax.need[j][0], r)) mode = 8;  // includes p == 0 (D5)
-      else if (cfg.strategy == 1) mode = bit8(ax.need[j][1], r) ? 16 : 12;
+      else if (bitw(ax.sel[j], r)) mode = 0;
+      else if (!bitw(ax.need[j][0], r)) mode = 8;  // includes p == 0 (D5)
+      else if (cfg.strategy == 1) mode = bitw(ax.need[j][1], r) ? 16 : 12;
       else mode = 1;
       uint32_t w[4];
       uint32_t clo = 0, chi = 0;
       if (mode == 0) {
-        if (EXPORT && vt) *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(0x10101010u, 0x10101010u);
+        if (EXPORT && vt)
+          *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(0x10101010u, 0x10101010u);
         continue;
       } else if (mode != 1) {
-        const TierMask tm = tier_mask(mode);
-        assemble8(h.x, h.y, bsel(tm.mk, mv, 0x88888888u), bsel(tm.lk, lv, tm.lf), w);
-        if (aligned && mode != 8) {
-          adj[j][0] -= 8;
-          if (mode == 12) adj[j][1] += 8;
-          else adj[j][2] += 8;
+        if (mode == 8) {
+          t8_words(h, w);
+        } else {
+          const TierMask tm = tier_mask(mode);
+          assemble8(h.x, h.y, bsel(tm.mk, mv, 0x88888888u), bsel(tm.lk, lv, tm.lf), w);
+          if (aligned) {
+            adj[j][0] -= 8;
+            if (mode == 12) adj[j][1] += 8;
+            else adj[j][2] += 8;
+          }
         }
         if (EXPORT) clo = chi = (uint32_t)mode * 0x01010101u;
       } else {
@@ -309,70 +335,17 @@ __device__ __forceinline__ void pv_consume(PvSmem<G>& sm, int stage, int grp, in
       if (EXPORT && vt) *reinterpret_cast<uint2*>(vt + j * (size_t)cap * D + (size_t)r * D) = make_uint2(clo, chi);
     }
   }
-  // base counts: every valid unselected row at T8 (aligned) or at the uniform tier
-  if (w4 == 0 && lane < G) {
-    const int j = lane;
-    int nsel = 0;
-    if (aligned) {
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int lo = w * 32, valid = min(max(rows - lo, 0), 32);
-        const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-        nsel += __popc(ax.sel[j][w] & vm);
-      }
-    }
-    const int base = (rows - nsel) * D;
-    if (aligned || uni == 8) adj[j][0] += base;
-    else if (uni == 12) adj[j][1] += base;
-    else adj[j][2] += base;
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
-
-  // partial o: half-warps -> warps (shared) -> page
-  float* red = &sm.red[grp][w4][0][0];
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      acc[j][k].x += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].x, 16);
-      acc[j][k].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][k].y, 16);
-    }
-    if (half == 0) {
-      float4* dst = reinterpret_cast<float4*>(red + j * D + cl * 8);
-      dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
-      dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
-    }
-    const int a = warp_sum_i(adj[j][0]), b = warp_sum_i(adj[j][1]), c = warp_sum_i(adj[j][2]);
-    if (lane == 0) {
-      unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + ((size_t)u * G + j) * 8 + 3);
-      if (a) atomicAdd(ct + 0, (unsigned long long)(long long)a);
-      if (b) atomicAdd(ct + 1, (unsigned long long)(long long)b);
-      if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
-    }
-  }
-  named_bar(1 + grp, 128);
-  for (int j = w4; j < G; j += 4) {
-    const float4 a = *reinterpret_cast<const float4*>(&sm.red[grp][0][j][lane * 4]);
-    const float4 b = *reinterpret_cast<const float4*>(&sm.red[grp][1][j][lane * 4]);
-    const float4 c = *reinterpret_cast<const float4*>(&sm.red[grp][2][j][lane * 4]);
-    const float4 d = *reinterpret_cast<const float4*>(&sm.red[grp][3][j][lane * 4]);
-    const float4 o = make_float4((a.x + b.x) + (c.x + d.x), (a.y + b.y) + (c.y + d.y), (a.z + b.z) + (c.z + d.z),
-                                 (a.w + b.w) + (c.w + d.w));
-    *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + lane * 4) = o;
-  }
-  named_bar(1 + grp, 128);
 }
 
 template <int G, bool TRUNC, bool EXPORT>
 __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st,
                                                                     int cap, int npg_max) {
-  constexpr int NS = PvShape<G>::NS, NG = PvShape<G>::NG;
+  constexpr int NG = PvShape<G>::NG, PV_NS = PvShape<G>::NS;
   extern __shared__ __align__(128) uint8_t pv_smem_raw[];
   PvSmem<G>& sm = *reinterpret_cast<PvSmem<G>*>(pv_smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) {
+    for (int i = 0; i < PV_NS; ++i) {
       mbar_init(&sm.full[i], 33);  // expect_tx arrival + 32 cp.async arrivals
       mbar_init(&sm.empty[i], 4);
     }
@@ -383,38 +356,107 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
   const bool uniform = cfg.force_tier != 0 || TRUNC;
 
   if (warp == 0) {
-    // ---------------- producer: static strided item schedule, loads one item ahead ----------------
-    PvPrefetch cur, nxt;
-    long long idx = blockIdx.x;
-    pv_fetch<G>(nxt, s, cfg, st, npg_max, idx, total, cap, uniform);
+    // ---------------- producer: contiguous item range, need bits one page ahead ----------------
+    const long long per = (total + gridDim.x - 1) / gridDim.x;
+    const long long i0 = (long long)blockIdx.x * per, i1 = min(total, i0 + per);
     int k = 0;
-    for (;;) {
+    PvPage cur, nxt;
+    auto advance = [&](long long from, PvPage& f) -> long long {
+      for (long long idx = from; idx < i1; ++idx) {
+        const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
+        const int n = s.lengths[u];
+        if (pg * P >= n) continue;
+        pv_fetch<G>(f, cfg, st, u, pg, n, cap, uniform);
+        return idx;
+      }
+      return -1;
+    };
+    long long nidx = advance(i0, nxt);
+    while (nidx >= 0) {
+      const long long idx = nidx;
       cur = nxt;
-      if (cur.item < 0) break;
-      idx += gridDim.x;
-      pv_fetch<G>(nxt, s, cfg, st, npg_max, idx, total, cap, uniform);
-      if (cur.pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
-      const int stage = k % NS;
-      mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
-      pv_produce<G>(sm, cur, stage, s, st, cap);
-      ++k;
+      nidx = advance(idx + 1, nxt);  // prefetch the next page's need bits
+      const int pg = (int)(idx % npg_max);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf, ++k) {
+        const int stage = k % PV_NS;
+        mbar_wait(&sm.empty[stage], ((k / PV_NS) & 1) ^ 1);
+        pv_stage<G>(sm, stage, hf, (int)idx, pg, cur, s, st, cap);
+      }
     }
-    for (int t = 0; t < NG; ++t, ++k) {
-      const int stage = k % NS;
-      mbar_wait(&sm.empty[stage], ((k / NS) & 1) ^ 1);
+    for (int t = 0; t < 2 * NG; ++t, ++k) {
+      const int stage = k % PV_NS;
+      mbar_wait(&sm.empty[stage], ((k / PV_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
       __syncwarp();
-      mbar_arrive(&sm.full[stage]);  // 32 lane arrivals ...
+      mbar_arrive(&sm.full[stage]);                 // 32 lane arrivals ...
       if (lane == 0) mbar_arrive(&sm.full[stage]);  // ... + the expect_tx slot
       __syncwarp();
     }
   } else {
     const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
-    for (int k = grp;; k += NG) {
-      const int stage = k % NS;
-      mbar_wait(&sm.full[stage], (k / NS) & 1);
-      if (sm.meta[stage].item < 0) break;
-      pv_consume<G, TRUNC, EXPORT>(sm, stage, grp, w4, cfg, st, cap);
+    for (int kp = grp;; kp += NG) {
+      float2 acc[G][4];
+      int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8"
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        adj[j][0] = adj[j][1] = adj[j][2] = 0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) acc[j][kk] = make_float2(0.f, 0.f);
+      }
+      int u = 0, pg = 0;
+      bool done = false;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int kk = 2 * kp + hf, stage = kk % PV_NS;
+        mbar_wait(&sm.full[stage], (kk / PV_NS) & 1);
+        if (sm.meta[stage].item < 0) {
+          done = true;
+          break;
+        }
+        if (hf == 0) {
+          u = sm.meta[stage].u;
+          pg = sm.meta[stage].pg;
+        }
+        pv_consume_half<G, TRUNC, EXPORT>(sm, stage, w4, cfg, st, cap, acc, adj);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
+      }
+      if (done) break;
+      // partial o of the page: half-warps -> warps (shared) -> page
+      const int half = lane >> 4, cl = lane & 15;
+      float* red = &sm.red[grp][w4][0][0];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          acc[j][kk].x += __shfl_xor_sync(0xFFFFFFFFu, acc[j][kk].x, 16);
+          acc[j][kk].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][kk].y, 16);
+        }
+        if (half == 0) {
+          float4* dst = reinterpret_cast<float4*>(red + j * D + cl * 8);
+          dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+          dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
+        }
+        const int a = warp_sum_i(adj[j][0]), b = warp_sum_i(adj[j][1]), c = warp_sum_i(adj[j][2]);
+        if (lane == 0) {
+          unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + ((size_t)u * G + j) * 8 + 3);
+          if (a) atomicAdd(ct + 0, (unsigned long long)(long long)a);
+          if (b) atomicAdd(ct + 1, (unsigned long long)(long long)b);
+          if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
+        }
+      }
+      named_bar(1 + grp, 128);
+      for (int j = w4; j < G; j += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(&sm.red[grp][0][j][lane * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&sm.red[grp][1][j][lane * 4]);
+        const float4 c = *reinterpret_cast<const float4*>(&sm.red[grp][2][j][lane * 4]);
+        const float4 d = *reinterpret_cast<const float4*>(&sm.red[grp][3][j][lane * 4]);
+        const float4 o = make_float4((a.x + b.x) + (c.x + d.x), (a.y + b.y) + (c.y + d.y),
+                                     (a.z + b.z) + (c.z + d.z), (a.w + b.w) + (c.w + d.w));
+        *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + lane * 4) = o;
+      }
+      named_bar(1 + grp, 128);
     }
   }
 }

@@ -1,22 +1,25 @@
 // scores_aligned for every (unit, q-head) of a batch.
 //
-// Warp-specialised persistent kernel, one CTA per SM:
+// Warp-specialised persistent kernel, one CTA per SM, 6-stage shared ring of
+// half pages (64 channels x 256 tokens: 16 KB head plane + up to 8 KB mid +
+// 8 KB low rows), two half-page stages per page:
 //
-//  producer warp   walks a contiguous range of (unit, page) items, evaluates Rule 1 for the unit's q-heads
-//                  (rule1_target SPEC.md:157-165, required_mantissa_bits
-//                  :139-147, tier_for_bits :148-156, k_channel_tiers :175-183,
-//                  SURVEY App. A A-K/D1/D2/D8) once per unit (the next unit's q and
-//                  ColMax are prefetched), publishes the channel list and
-//                  tier codes, and streams the page into a 3-stage shared
-//                  ring with TMA bulk copies (cp.async.bulk + mbarrier
-//                  complete_tx): the whole 32 KB head plane in one copy, and
-//                  only the 128 B mid / low channel rows whose union
-//                  tier needs them (SKIP / T8 channels read 8 bits or nothing);
-//                  (rows fetched by cp.async from all 32 lanes: TMA pays a
-//                  fixed cost per bulk copy, too high for 128 B rows);
+//  producer warp   walks a contiguous range of (unit, page) items, evaluates
+//                  Rule 1 for the unit's q-heads once per unit (rule1_target
+//                  SPEC.md:157-165, required_mantissa_bits :139-147,
+//                  tier_for_bits :148-156, k_channel_tiers :175-183, SURVEY
+//                  App. A A-K/D1/D2/D8; the next unit's q and ColMax are
+//                  prefetched), builds per half a channel list ordered by union
+//                  class (T8 first, then T12/T16; SKIP channels dropped), and
+//                  fills the stage: the 16 KB head-plane half by one TMA bulk
+//                  copy (cp.async.bulk + mbarrier complete_tx) and only the
+//                  128 B mid / low channel rows the union tier needs by
+//                  cp.async from all 32 lanes (TMA pays a fixed cost per bulk
+//                  copy, too high for 128 B rows);
 //  2 x 4 consumer  warps (two pages in flight) rebuild the fp16 words from
 //                  shared memory with PRMT/LOP3 (midpoint fill for absent
-//                  nibbles, HB:160-179) and accumulate q_c * K~ with the
+//                  nibbles, HB:160-179) in two branch-free loops (T8 class,
+//                  T12/T16 class) and accumulate q_c * K~ with the
 //                  mixed-precision FHFMA (exact fp16 x fp16 products, fp32
 //                  sums, D9); the 1/sqrt(d) scale is applied
 //                  after accumulation; each page also yields its
@@ -24,16 +27,19 @@
 //
 // Work split inside a consumer group: G = 1, 2 split the channel list (4 or 2
 // ways) and reduce partial sums through shared memory; G >= 4 give every warp
-// G/4 heads over all channels (no reduction).  Results do not depend on which
-// CTA / group processes a page, so the kernel is deterministic.
+// G/4 heads over all channels.  Each page's result is independent of which CTA
+// or group computes it: the kernel is deterministic.
 #include <algorithm>
 
 #include "akv_common.cuh"
 
 namespace akv {
 
-constexpr int QK_NS = 3;                         // ring stages
-constexpr int QK_THREADS = 32 * 9;               // 1 producer + 8 consumer warps
+constexpr int QK_NS = 6;                 // ring stages (half pages)
+constexpr int QK_THREADS = 32 * 9;       // 1 producer + 8 consumer warps
+constexpr int HCH = D / 2;               // channels per half page
+constexpr int QS = HCH * P * 2;          // 32 KB stage: head [64][256] | mid [64][128] | low [64][128]
+constexpr int QS_MID = HCH * P, QS_LOW = HCH * P + HCH * (P / 2);
 
 template <int E, int Q>
 __device__ __forceinline__ float fma_hh(uint32_t a, uint32_t qpair, float c) {
@@ -69,23 +75,22 @@ __device__ __forceinline__ void fma8(const uint32_t w[4], uint32_t qpair, float 
   acc[7] = fma_hh<1, Q>(w[3], qpair, acc[7]);
 }
 
-// Per-stage metadata published by the producer (list order: T8 class first).
+// Per-stage (half page) metadata; list order: T8 class first, both ranges padded to 8.
 template <int G>
 struct alignas(16) QkMeta {
   int item, u, pg, n;
-  int n8p, nlist, pad1, pad2;  // T8-class range [0, n8p), full range [n8p, nlist); both padded to 8
-  uint16_t ent[D + 8];      // channel | has_low << 8 (pads: channel 0, q = 0)
-  uint32_t q[G][D / 2 + 4]; // q (fp16) per list position, pairs; 0 for SKIP heads / pads
-  uint8_t code[G][D + 8];       // per-head read code per list position (8/12/16; SKIP -> 8 with q = 0)
+  int n8p, nlist, half, pad;
+  uint16_t ent[HCH + 8];        // local channel (0..63) | has_low << 8 ; pads: channel 0, q = 0
+  uint32_t q[G][HCH / 2 + 4];   // q (fp16) per list position, pairs; 0 for SKIP heads / pads
+  uint8_t code[G][HCH + 8];     // per-head read code per list position (8/12/16; SKIP -> 8 with q = 0)
 };
 
 template <int G>
 struct alignas(128) QkSmem {
-  uint8_t data[QK_NS][PAGE];
+  uint8_t data[QK_NS][QS];
   QkMeta<G> meta[QK_NS];
-  QkMeta<G> cache;           // producer-private: the current unit's list (copied into each stage)
+  QkMeta<G> cache[2];        // producer-private: the current unit's lists (one per half)
   float red[2][4][P];        // partial token sums per group / warp (channel split, G <= 2)
-  float stat[2][4][2];
   uint64_t full[QK_NS], empty[QK_NS];
 };
 
@@ -124,15 +129,15 @@ __device__ __forceinline__ void qk_fetch_unit(QkUnit<G>& f, const akv_store_t& s
     for (int k = 0; k < 4; ++k) f.qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
 }
 
-// Rule 1 for one unit (all q-heads): tier codes, the channel list and the
+// Rule 1 for one unit (all q-heads): tier codes, the two half lists and the
 // fetch masks; once per unit per CTA.  `book`: this CTA owns the unit's page 0
 // and writes the per-step bookkeeping (K tiers, K counters, status, bytes).
+// Lane l owns channels l + 32k (k = 0..3): words k = 0, 1 are half 0.
 template <int G, bool TRUNC>
 __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, const akv_cfg_t& cfg,
                                  const akv_step_t& st, uint32_t (&bm)[4], uint32_t (&bl)[4]) {
   const int lane = threadIdx.x & 31;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
-  QkMeta<G>& mt = sm.cache;
   int code[G][4], ucode[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -168,7 +173,7 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
       code[j][k] = cd;
       ucode[k] = max(ucode[k], cd);
     }
-    if (book) {  // per-step bookkeeping, once per unit (the page-0 item)
+    if (book) {  // per-step bookkeeping, once per unit
       const size_t h = (size_t)f.u * G + j;
       int c8 = 0, c12 = 0, c16 = 0, bad = 0;
 #pragma unroll
@@ -192,80 +197,85 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
       }
     }
   }
-  // channel list (T8 class first, then T12/T16; ascending channel inside a class)
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t b8[4];
-  int n8 = 0, nm = 0, nlo = 0;
+  int nh = 0, nm_all = 0, nl_all = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     b8[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 8);
     bm[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
     bl[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 16);
-    n8 += __popc(b8[k]);
-    nm += __popc(bm[k]);
-    nlo += __popc(bl[k]);
+    nh += __popc(b8[k]) + __popc(bm[k]);
+    nm_all += __popc(bm[k]);
+    nl_all += __popc(bl[k]);
   }
-  const int nl = n8 + nm;
-  const int n8p = (n8 + 7) & ~7, nlp = n8p + ((nm + 7) & ~7);
-  int base8 = 0, basem = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int c = lane + 32 * k;
-    int pos = -1;
-    if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
-    else if (ucode[k] >= 12) pos = n8p + basem + __popc(bm[k] & lt);
-    if (pos >= 0) {
-      mt.ent[pos] = (uint16_t)(c | ((ucode[k] == 16 ? 1 : 0) << 8));
+  for (int hf = 0; hf < 2; ++hf) {
+    QkMeta<G>& mt = sm.cache[hf];
+    const int n8 = __popc(b8[2 * hf]) + __popc(b8[2 * hf + 1]);
+    const int nm = __popc(bm[2 * hf]) + __popc(bm[2 * hf + 1]);
+    const int n8p = (n8 + 7) & ~7, nlp = n8p + ((nm + 7) & ~7);
+    int base8 = 0, basem = 0;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        reinterpret_cast<uint16_t*>(mt.q[j])[pos] = code[j][k] ? (uint16_t)f.qw[j][k] : (uint16_t)0;
-        mt.code[j][pos] = (uint8_t)(code[j][k] ? code[j][k] : 8);
+    for (int kk = 0; kk < 2; ++kk) {
+      const int k = 2 * hf + kk;
+      const int cl = lane + 32 * kk;  // channel inside the half
+      int pos = -1;
+      if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
+      else if (ucode[k] >= 12) pos = n8p + basem + __popc(bm[k] & lt);
+      if (pos >= 0) {
+        mt.ent[pos] = (uint16_t)(cl | ((ucode[k] == 16 ? 1 : 0) << 8));
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          reinterpret_cast<uint16_t*>(mt.q[j])[pos] = code[j][k] ? (uint16_t)f.qw[j][k] : (uint16_t)0;
+          mt.code[j][pos] = (uint8_t)(code[j][k] ? code[j][k] : 8);
+        }
+      }
+      base8 += __popc(b8[k]);
+      basem += __popc(bm[k]);
+    }
+    // pads (channel 0, q = 0): the head plane is always resident, so the word is finite and adds 0
+    if (lane < 8) {
+      const int p0 = n8 + lane, p1 = n8p + nm + lane;
+      if (p0 < n8p) {
+        mt.ent[p0] = 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          reinterpret_cast<uint16_t*>(mt.q[j])[p0] = 0;
+          mt.code[j][p0] = 8;
+        }
+      }
+      if (p1 < nlp) {
+        mt.ent[p1] = 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          reinterpret_cast<uint16_t*>(mt.q[j])[p1] = 0;
+          mt.code[j][p1] = 8;
+        }
       }
     }
-    base8 += __popc(b8[k]);
-    basem += __popc(bm[k]);
-  }
-  // pads (channel 0, q = 0): the head plane is always resident, so the word is finite and adds 0
-  if (lane < 8) {
-    const int p0 = n8 + lane, p1 = n8p + nm + lane;
-    if (p0 < n8p) {
-      mt.ent[p0] = 0;
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        reinterpret_cast<uint16_t*>(mt.q[j])[p0] = 0;
-        mt.code[j][p0] = 8;
-      }
-    }
-    if (p1 < nlp) {
-      mt.ent[p1] = 0;
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        reinterpret_cast<uint16_t*>(mt.q[j])[p1] = 0;
-        mt.code[j][p1] = 8;
-      }
+    if (lane == 0) {
+      mt.n8p = n8p;
+      mt.nlist = nlp;
+      mt.half = hf;
     }
   }
   if (book && lane == 0) {
-    st.unit_bytes[(size_t)f.u * 4 + 0] = (int64_t)f.n * nl + (int64_t)(f.n / 2) * (nm + nlo);
+    st.unit_bytes[(size_t)f.u * 4 + 0] = (int64_t)f.n * nh + (int64_t)(f.n / 2) * (nm_all + nl_all);
     st.unit_bytes[(size_t)f.u * 4 + 1] = 0;
-  }
-  (void)nl;
-  if (lane == 0) {
-    mt.n8p = n8p;
-    mt.nlist = nlp;
   }
   __syncwarp();
 }
 
-// Publish one page into a ring stage: the cached unit list + item fields, then
-// the copies (head plane by TMA bulk copy; needed mid / low rows by cp.async).
+// Publish one half page into a ring stage: the cached half list + item fields,
+// then the copies (head half by TMA bulk copy; needed mid / low rows by cp.async).
 template <int G>
-__device__ void qk_stage(QkSmem<G>& sm, int stage, int item, int u, int pg, int n, const akv_store_t& s,
+__device__ void qk_stage(QkSmem<G>& sm, int stage, int hf, int item, int u, int pg, int n, const akv_store_t& s,
                          const uint32_t (&bm)[4], const uint32_t (&bl)[4]) {
   const int lane = threadIdx.x & 31;
   QkMeta<G>& mt = sm.meta[stage];
   constexpr int W = sizeof(QkMeta<G>) / 16;
-  const uint4* srcm = reinterpret_cast<const uint4*>(&sm.cache);
+  const uint4* srcm = reinterpret_cast<const uint4*>(&sm.cache[hf]);
   uint4* dstm = reinterpret_cast<uint4*>(&mt);
   for (int i = lane; i < W; i += 32) dstm[i] = srcm[i];
   __syncwarp();
@@ -279,11 +289,13 @@ __device__ void qk_stage(QkSmem<G>& sm, int stage, int item, int u, int pg, int 
   uint8_t* dst = sm.data[stage];
   __syncwarp();
   if (lane == 0) {
-    mbar_arrive_expect_tx(&sm.full[stage], D * P);
-    bulk_g2s(dst, src, D * P, &sm.full[stage]);
+    mbar_arrive_expect_tx(&sm.full[stage], HCH * P);
+    bulk_g2s(dst, src + hf * HCH * P, HCH * P, &sm.full[stage]);
   }
-  cp_rows<4, P / 2>(bm, dst + MID, src + MID);
-  cp_rows<4, P / 2>(bl, dst + LOW, src + LOW);
+  const uint32_t mm[2] = {bm[2 * hf], bm[2 * hf + 1]};
+  const uint32_t ml[2] = {bl[2 * hf], bl[2 * hf + 1]};
+  cp_rows<2, P / 2>(mm, dst + QS_MID, src + MID + hf * HCH * (P / 2));
+  cp_rows<2, P / 2>(ml, dst + QS_LOW, src + LOW + hf * HCH * (P / 2));
   cp_async_arrive_noinc(&sm.full[stage]);
 }
 
@@ -291,25 +303,19 @@ __device__ void qk_stage(QkSmem<G>& sm, int stage, int item, int u, int pg, int 
 // consumer
 // ----------------------------------------------------------------------------
 template <int G, bool TRUNC>
-__device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, int w4, const akv_store_t& s,
-                                           const akv_step_t& st, int cap, float isd, uint32_t tkm, uint32_t tf) {
+__device__ __forceinline__ void qk_consume_half(const QkSmem<G>& sm, int stage, int w4, float (&acc)[QkSplit<G>::HW][8],
+                                                uint32_t tkm, uint32_t tf) {
   constexpr int CS = QkSplit<G>::CS, HW = QkSplit<G>::HW;
   const int lane = threadIdx.x & 31;
   const QkMeta<G>& mt = sm.meta[stage];
   const uint8_t* pgd = sm.data[stage];
   const int cs = w4 % CS;
-  const int j0 = (w4 / CS) * HW;  // first head of this warp
+  const int j0 = (w4 / CS) * HW;
   const int nb8 = mt.n8p >> 3, nb = mt.nlist >> 3;
-  const int u = mt.u, pg = mt.pg, n = mt.n;  // read before the stage is released
-  float acc[HW][8];
-#pragma unroll
-  for (int jj = 0; jj < HW; ++jj)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[jj][e] = 0.f;
   const uint8_t* hb = pgd + lane * 8;
-  const uint8_t* mb = pgd + MID + lane * 4;
+  const uint8_t* mb = pgd + QS_MID + lane * 4;
 
-  // T8-class channels: head byte only (all q-heads read T8 or SKIP with q = 0)
+  // T8-class channels: head byte only (every q-head reads T8, or SKIP with q = 0)
   for (int b = cs; b < nb8; b += CS) {
     const uint4 e4 = *reinterpret_cast<const uint4*>(&mt.ent[b * 8]);
 #pragma unroll
@@ -345,7 +351,7 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
       const uint2 h = *reinterpret_cast<const uint2*>(hb + ch * P);
       const uint32_t m = *reinterpret_cast<const uint32_t*>(mb + ch * (P / 2));
       uint32_t l = 0x88888888u;
-      if (en >> 8) l = *reinterpret_cast<const uint32_t*>(mb + (LOW - MID) + ch * (P / 2));
+      if (en >> 8) l = *reinterpret_cast<const uint32_t*>(mb + (QS_LOW - QS_MID) + ch * (P / 2));
       uint32_t w[4];
       assemble8(h.x, h.y, m, l, w);
       if (TRUNC) {
@@ -372,72 +378,48 @@ __device__ __forceinline__ void qk_consume(QkSmem<G>& sm, int stage, int grp, in
       }
     }
   }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage data no longer read by this warp
+}
 
+template <int G>
+__device__ __forceinline__ void qk_finish(int u, int pg, int n, int j, const float* sv8, const akv_store_t& s,
+                                          const akv_step_t& st, int cap, float isd) {
+  const int lane = threadIdx.x & 31;
   const int tok0 = pg * P + lane * 8;
   const int nv = min(max(n - tok0, 0), 8);
-  auto finish = [&](int j, const float* sv8) {
-    const size_t hh = (size_t)u * G + j;
-    float sv[8];
-    float m = -INFINITY;
+  const size_t hh = (size_t)u * G + j;
+  float sv[8];
+  float m = -INFINITY;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      sv[e] = sv8[e] * isd;
-      if (e < nv) m = fmaxf(m, sv[e]);
-    }
-    m = warp_max(m);
-    float l = 0.f;
+  for (int e = 0; e < 8; ++e) {
+    sv[e] = sv8[e] * isd;
+    if (e < nv) m = fmaxf(m, sv[e]);
+  }
+  m = warp_max(m);
+  float l = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (e < nv) l += expf(sv[e] - m);
+  l = warp_sum(l);
+  float* out = st.scores + hh * cap + tok0;
+  if (nv == 8) {
+    reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+    reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
+  } else {
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      if (e < nv) l += expf(sv[e] - m);
-    l = warp_sum(l);
-    float* out = st.scores + hh * cap + tok0;
-    if (nv == 8) {
-      reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-      reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e < nv) out[e] = sv[e];
-    }
-    if (lane == 0) {
-      float* ps = st.page_stats + (hh * s.max_pages + pg) * 2;
-      ps[0] = m;
-      ps[1] = l;
-    }
-  };
-  if (CS == 1) {
-#pragma unroll
-    for (int jj = 0; jj < HW; ++jj) finish(j0 + jj, acc[jj]);
-  } else {
-    // G == 1 (4-way channel split) or G == 2 (2 heads x 2-way split): reduce via shared memory
-    const int j = w4 / CS;
-    float* rw = sm.red[grp][w4];
-    *reinterpret_cast<float4*>(rw + lane * 8) = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
-    *reinterpret_cast<float4*>(rw + lane * 8 + 4) = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
-    named_bar(1 + grp, 128);
-    if (cs == 0) {
-      float sum[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) sum[e] = 0.f;
-#pragma unroll
-      for (int c2 = 0; c2 < CS; ++c2) {  // fixed order
-        const float* r2 = sm.red[grp][w4 + c2] + lane * 8;
-        const float4 a = *reinterpret_cast<const float4*>(r2);
-        const float4 bq = *reinterpret_cast<const float4*>(r2 + 4);
-        sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
-        sum[4] += bq.x; sum[5] += bq.y; sum[6] += bq.z; sum[7] += bq.w;
-      }
-      finish(j, sum);
-    }
-    named_bar(1 + grp, 128);
+      if (e < nv) out[e] = sv[e];
+  }
+  if (lane == 0) {
+    float* ps = st.page_stats + (hh * s.max_pages + pg) * 2;
+    ps[0] = m;
+    ps[1] = l;
   }
 }
 
 template <int G, bool TRUNC>
 __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap,
                                                            float isd, int npg_max) {
+  constexpr int CS = QkSplit<G>::CS, HW = QkSplit<G>::HW;
   extern __shared__ __align__(128) uint8_t qk_smem_raw[];
   QkSmem<G>& sm = *reinterpret_cast<QkSmem<G>*>(qk_smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,23 +451,25 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
         if (cur.n > 0) qk_unit_prologue<G, TRUNC>(sm, cur, pg == 0, cfg, st, bm, bl);
       }
       if (pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
-      const int stage = k % QK_NS;
-      mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
-      qk_stage<G>(sm, stage, (int)idx, u, pg, cur.n, s, bm, bl);
-      ++k;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf, ++k) {
+        const int stage = k % QK_NS;
+        mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
+        qk_stage<G>(sm, stage, hf, (int)idx, u, pg, cur.n, s, bm, bl);
+      }
     }
-    // one terminator per consumer group
-    for (int t = 0; t < 2; ++t, ++k) {
+    // terminators: the next page slot of each consumer group (both halves)
+    for (int t = 0; t < 4; ++t, ++k) {
       const int stage = k % QK_NS;
       mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
       __syncwarp();
-      mbar_arrive(&sm.full[stage]);  // 32 lane arrivals ...
+      mbar_arrive(&sm.full[stage]);                 // 32 lane arrivals ...
       if (lane == 0) mbar_arrive(&sm.full[stage]);  // ... + the expect_tx slot
       __syncwarp();
     }
   } else {
-    // ---------------- consumers: two groups of four warps ----------------
+    // ---------------- consumers: two groups of four warps, one page each ----------------
     const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
     uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
     if (TRUNC) {
@@ -495,11 +479,58 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
       tkm = km | (km << 16);
       tf = fill | (fill << 16);
     }
-    for (int k = grp;; k += 2) {
-      const int stage = k % QK_NS;
-      mbar_wait(&sm.full[stage], (k / QK_NS) & 1);
-      if (sm.meta[stage].item < 0) break;
-      qk_consume<G, TRUNC>(sm, stage, grp, w4, s, st, cap, isd, tkm, tf);
+    const int cs = w4 % CS, j0 = (w4 / CS) * HW;
+    for (int kp = grp;; kp += 2) {
+      float acc[HW][8];
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[jj][e] = 0.f;
+      int u = 0, pg = 0, n = 0;
+      bool done = false;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int kk = 2 * kp + hf, stage = kk % QK_NS;
+        mbar_wait(&sm.full[stage], (kk / QK_NS) & 1);
+        if (sm.meta[stage].item < 0) {
+          done = true;
+          break;
+        }
+        if (hf == 0) {
+          u = sm.meta[stage].u;
+          pg = sm.meta[stage].pg;
+          n = sm.meta[stage].n;
+        }
+        qk_consume_half<G, TRUNC>(sm, stage, w4, acc, tkm, tf);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
+      }
+      if (done) break;
+      if (CS == 1) {
+#pragma unroll
+        for (int jj = 0; jj < HW; ++jj) qk_finish<G>(u, pg, n, j0 + jj, acc[jj], s, st, cap, isd);
+      } else {
+        // channel split (G <= 2): reduce the partial sums of the CS warps of each head, fixed order
+        float* rw = sm.red[grp][w4];
+        *reinterpret_cast<float4*>(rw + lane * 8) = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+        *reinterpret_cast<float4*>(rw + lane * 8 + 4) = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+        named_bar(1 + grp, 128);
+        if (cs == 0) {
+          float sum[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sum[e] = 0.f;
+#pragma unroll
+          for (int c2 = 0; c2 < CS; ++c2) {
+            const float* r2 = sm.red[grp][w4 + c2] + lane * 8;
+            const float4 a = *reinterpret_cast<const float4*>(r2);
+            const float4 bq = *reinterpret_cast<const float4*>(r2 + 4);
+            sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
+            sum[4] += bq.x; sum[5] += bq.y; sum[6] += bq.z; sum[7] += bq.w;
+          }
+          qk_finish<G>(u, pg, n, j0, sum, s, st, cap, isd);
+        }
+        named_bar(1 + grp, 128);
+      }
     }
   }
 }
