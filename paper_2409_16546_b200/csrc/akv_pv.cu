@@ -12,12 +12,11 @@
 //                  64 B mid / low rows some q-head of the kv-head needs, and
 //                  the per-row metadata (p_t, selection bits, need bits,
 //                  rule-2 targets), by cp.async from all 32 lanes;
-//  consumer warps  (two groups of four for G <= 2, one group for G >= 4):
-//                  16 lanes per row x 8 channels per lane, two rows per warp
-//                  instruction, 32 rows per warp per half page.  A per-half
+//  8 consumer      warps: 16 lanes per row x 8 channels per lane, two rows per
+//                  warp instruction, 16 rows per warp per half page.  A per-half
 //                  pre-pass folds the selection (D6: selected rows' T16
 //                  contribution is already in o_est) and the page end into p.
-//                  A 32-row block that no q-head needs beyond T8 takes a
+//                  A 16-row block that no q-head needs beyond T8 takes a
 //                  branch-free unrolled path (4 PRMT per 8 elements); other
 //                  rows apply each head's rule: p_t = 0 -> T8 (D5); ELEMENT:
 //                  keep mid iff max(bexp,1) + e(p_t) > 17 + target_r - margin,
@@ -40,9 +39,8 @@ constexpr int VS_MID = HR * D, VS_LOW = HR * D + HR * (D / 2);
 
 template <int G>
 struct PvShape {
-  static constexpr int NG = G >= 4 ? 1 : 2;  // consumer groups (pages in flight)
-  static constexpr int NS = G >= 8 ? 4 : 6;  // ring stages (half pages)
-  static constexpr int THREADS = 32 * (1 + 4 * NG);
+  static constexpr int NS = G >= 4 ? 4 : 6;  // ring stages (half pages; shared memory bound for G >= 4)
+  static constexpr int THREADS = 32 * 9;       // 1 producer + 8 consumer warps
 };
 
 template <int G>
@@ -64,7 +62,7 @@ struct alignas(128) PvSmem {
   uint8_t data[PvShape<G>::NS][VS];
   PvAux<G> aux[PvShape<G>::NS];
   PvMeta meta[PvShape<G>::NS];
-  float red[PvShape<G>::NG][4][G][D];
+  float red[8][G][D];
   uint64_t full[PvShape<G>::NS], empty[PvShape<G>::NS];
 };
 
@@ -185,7 +183,7 @@ __device__ void pv_stage(PvSmem<G>& sm, int stage, int hf, int item, int pg, con
 // consumer
 // ----------------------------------------------------------------------------
 template <int G, bool TRUNC, bool EXPORT>
-__device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4, const akv_cfg_t& cfg,
+__device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w8, const akv_cfg_t& cfg,
                                                 const akv_step_t& st, int cap, float2 (&acc)[G][4],
                                                 int (&adj)[G][3]) {
   const int lane = threadIdx.x & 31;
@@ -207,10 +205,10 @@ __device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4
   uint8_t* vt = (EXPORT && st.v_tiers)
                     ? st.v_tiers + ((size_t)u * G * cap + (size_t)pg * P + (size_t)hf * HR) * D + cl * 8
                     : nullptr;
-  const int r0 = w4 * 32;  // this warp's 32 rows inside the half
+  const int r0 = w8 * 16;  // this warp's 16 rows inside the half
 
   // base counts: every valid unselected row at T8 (aligned) or at the uniform tier
-  if (w4 == 0 && lane < G) {
+  if (w8 == 0 && lane < G) {
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       if (j != lane) continue;
@@ -231,19 +229,19 @@ __device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4
   }
   if (r0 >= rows) return;
   // pre-pass: fold the selection (D6) and the page end into p (0 -> no contribution)
-  {
+  if (lane < 16) {
     const int r = r0 + lane;
 #pragma unroll
     for (int j = 0; j < G; ++j)
       if (r >= rows || (aligned && bitw(ax.sel[j], r))) ax.probs[j][r] = 0.f;
-    __syncwarp();
   }
-  const bool full_blk = r0 + 32 <= rows;
-  if (aligned && full_blk && mt.un_mid[w4] == 0) {
+  __syncwarp();
+  const bool full_blk = r0 + 16 <= rows;
+  if (aligned && full_blk && ((mt.un_mid[r0 >> 5] >> (r0 & 31)) & 0xFFFFu) == 0) {
     // fast block: every row is T8 (or p = 0) for every q-head
     const uint8_t* hp = pgd + (r0 + half) * D + cl * 8;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const uint2 h = *reinterpret_cast<const uint2*>(hp + i * 2 * D);
       uint32_t w[4];
       t8_words(h, w);
@@ -265,7 +263,7 @@ __device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4
     return;
   }
   // generic rows
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < 8; ++i) {
     const int r = r0 + 2 * i + half;
     if (r >= rows) continue;
     const uint2 h = *reinterpret_cast<const uint2*>(pgd + r * D + cl * 8);
@@ -340,7 +338,7 @@ __device__ __forceinline__ void pv_consume_half(PvSmem<G>& sm, int stage, int w4
 template <int G, bool TRUNC, bool EXPORT>
 __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st,
                                                                     int cap, int npg_max) {
-  constexpr int NG = PvShape<G>::NG, PV_NS = PvShape<G>::NS;
+  constexpr int PV_NS = PvShape<G>::NS;
   extern __shared__ __align__(128) uint8_t pv_smem_raw[];
   PvSmem<G>& sm = *reinterpret_cast<PvSmem<G>*>(pv_smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -384,7 +382,7 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
         pv_stage<G>(sm, stage, hf, (int)idx, pg, cur, s, st, cap);
       }
     }
-    for (int t = 0; t < 2 * NG; ++t, ++k) {
+    for (int t = 0; t < 2; ++t, ++k) {
       const int stage = k % PV_NS;
       mbar_wait(&sm.empty[stage], ((k / PV_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
@@ -394,8 +392,8 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
       __syncwarp();
     }
   } else {
-    const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
-    for (int kp = grp;; kp += NG) {
+    const int w8 = warp - 1;
+    for (int kp = 0;; ++kp) {
       float2 acc[G][4];
       int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8"
 #pragma unroll
@@ -418,14 +416,13 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
           u = sm.meta[stage].u;
           pg = sm.meta[stage].pg;
         }
-        pv_consume_half<G, TRUNC, EXPORT>(sm, stage, w4, cfg, st, cap, acc, adj);
+        pv_consume_half<G, TRUNC, EXPORT>(sm, stage, w8, cfg, st, cap, acc, adj);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }
       if (done) break;
       // partial o of the page: half-warps -> warps (shared) -> page
       const int half = lane >> 4, cl = lane & 15;
-      float* red = &sm.red[grp][w4][0][0];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
 #pragma unroll
@@ -434,7 +431,7 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
           acc[j][kk].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][kk].y, 16);
         }
         if (half == 0) {
-          float4* dst = reinterpret_cast<float4*>(red + j * D + cl * 8);
+          float4* dst = reinterpret_cast<float4*>(&sm.red[w8][j][cl * 8]);
           dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
           dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
         }
@@ -446,17 +443,20 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
           if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
         }
       }
-      named_bar(1 + grp, 128);
-      for (int j = w4; j < G; j += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(&sm.red[grp][0][j][lane * 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&sm.red[grp][1][j][lane * 4]);
-        const float4 c = *reinterpret_cast<const float4*>(&sm.red[grp][2][j][lane * 4]);
-        const float4 d = *reinterpret_cast<const float4*>(&sm.red[grp][3][j][lane * 4]);
-        const float4 o = make_float4((a.x + b.x) + (c.x + d.x), (a.y + b.y) + (c.y + d.y),
-                                     (a.z + b.z) + (c.z + d.z), (a.w + b.w) + (c.w + d.w));
+      named_bar(1, 256);
+      for (int j = w8; j < G; j += 8) {
+        float4 o = *reinterpret_cast<const float4*>(&sm.red[0][j][lane * 4]);
+#pragma unroll
+        for (int w = 1; w < 8; ++w) {  // fixed order
+          const float4 a = *reinterpret_cast<const float4*>(&sm.red[w][j][lane * 4]);
+          o.x += a.x;
+          o.y += a.y;
+          o.z += a.z;
+          o.w += a.w;
+        }
         *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + lane * 4) = o;
       }
-      named_bar(1 + grp, 128);
+      named_bar(1, 256);
     }
   }
 }

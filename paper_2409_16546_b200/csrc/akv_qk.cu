@@ -16,7 +16,7 @@
 //                  128 B mid / low channel rows the union tier needs by
 //                  cp.async from all 32 lanes (TMA pays a fixed cost per bulk
 //                  copy, too high for 128 B rows);
-//  2 x 4 consumer  warps (two pages in flight) rebuild the fp16 words from
+//  8 consumer      warps (the channel list split over them) rebuild the fp16 words from
 //                  shared memory with PRMT/LOP3 (midpoint fill for absent
 //                  nibbles, HB:160-179) in two branch-free loops (T8 class,
 //                  T12/T16 class) and accumulate q_c * K~ with the
@@ -25,9 +25,9 @@
 //                  after accumulation; each page also yields its
 //                  (max, sum exp) for the split softmax.
 //
-// Work split inside a consumer group: G = 1, 2 split the channel list (4 or 2
-// ways) and reduce partial sums through shared memory; G >= 4 give every warp
-// G/4 heads over all channels.  Each page's result is independent of which CTA
+// Work split over the 8 consumer warps: the channel list is split 8/G ways per
+// head and partial sums are reduced through shared memory in a fixed order;
+// G = 8 gives every warp one head over all channels.  Each page's result is independent of which CTA
 // or group computes it: the kernel is deterministic.
 #include <algorithm>
 
@@ -90,14 +90,14 @@ struct alignas(128) QkSmem {
   uint8_t data[QK_NS][QS];
   QkMeta<G> meta[QK_NS];
   QkMeta<G> cache[2];        // producer-private: the current unit's lists (one per half)
-  float red[2][4][P];        // partial token sums per group / warp (channel split, G <= 2)
+  float red[8][P];           // partial token sums per consumer warp (channel split)
   uint64_t full[QK_NS], empty[QK_NS];
 };
 
 template <int G>
 struct QkSplit {
-  static constexpr int CS = G >= 4 ? 1 : 4 / G;  // ways the channel list is split inside a group
-  static constexpr int HW = G >= 4 ? G / 4 : 1;  // heads per consumer warp
+  static constexpr int CS = G >= 8 ? 1 : 8 / G;  // ways the channel list is split over the 8 consumer warps
+  static constexpr int HW = G >= 8 ? G / 8 : 1;  // heads per consumer warp
 };
 
 __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
@@ -303,14 +303,14 @@ __device__ void qk_stage(QkSmem<G>& sm, int stage, int hf, int item, int u, int 
 // consumer
 // ----------------------------------------------------------------------------
 template <int G, bool TRUNC>
-__device__ __forceinline__ void qk_consume_half(const QkSmem<G>& sm, int stage, int w4, float (&acc)[QkSplit<G>::HW][8],
+__device__ __forceinline__ void qk_consume_half(const QkSmem<G>& sm, int stage, int w8, float (&acc)[QkSplit<G>::HW][8],
                                                 uint32_t tkm, uint32_t tf) {
   constexpr int CS = QkSplit<G>::CS, HW = QkSplit<G>::HW;
   const int lane = threadIdx.x & 31;
   const QkMeta<G>& mt = sm.meta[stage];
   const uint8_t* pgd = sm.data[stage];
-  const int cs = w4 % CS;
-  const int j0 = (w4 / CS) * HW;
+  const int cs = w8 % CS;
+  const int j0 = (w8 / CS) * HW;
   const int nb8 = mt.n8p >> 3, nb = mt.nlist >> 3;
   const uint8_t* hb = pgd + lane * 8;
   const uint8_t* mb = pgd + QS_MID + lane * 4;
@@ -458,8 +458,8 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
         qk_stage<G>(sm, stage, hf, (int)idx, u, pg, cur.n, s, bm, bl);
       }
     }
-    // terminators: the next page slot of each consumer group (both halves)
-    for (int t = 0; t < 4; ++t, ++k) {
+    // terminator: the next page slot (both halves)
+    for (int t = 0; t < 2; ++t, ++k) {
       const int stage = k % QK_NS;
       mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
       __syncwarp();
     }
   } else {
-    // ---------------- consumers: two groups of four warps, one page each ----------------
-    const int cw = warp - 1, grp = cw >> 2, w4 = cw & 3;
+    // ---------------- consumers: eight warps share each page ----------------
+    const int w8 = warp - 1;
     uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
     if (TRUNC) {
       const int kb = cfg.trunc_bits - 6;
@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
       tkm = km | (km << 16);
       tf = fill | (fill << 16);
     }
-    const int cs = w4 % CS, j0 = (w4 / CS) * HW;
-    for (int kp = grp;; kp += 2) {
+    const int cs = w8 % CS, j0 = (w8 / CS) * HW;
+    for (int kp = 0;; ++kp) {
       float acc[HW][8];
 #pragma unroll
       for (int jj = 0; jj < HW; ++jj)
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
           pg = sm.meta[stage].pg;
           n = sm.meta[stage].n;
         }
-        qk_consume_half<G, TRUNC>(sm, stage, w4, acc, tkm, tf);
+        qk_consume_half<G, TRUNC>(sm, stage, w8, acc, tkm, tf);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }
@@ -510,18 +510,18 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
 #pragma unroll
         for (int jj = 0; jj < HW; ++jj) qk_finish<G>(u, pg, n, j0 + jj, acc[jj], s, st, cap, isd);
       } else {
-        // channel split (G <= 2): reduce the partial sums of the CS warps of each head, fixed order
-        float* rw = sm.red[grp][w4];
+        // channel split: reduce the CS partial sums of each head in a fixed order
+        float* rw = sm.red[w8];
         *reinterpret_cast<float4*>(rw + lane * 8) = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
         *reinterpret_cast<float4*>(rw + lane * 8 + 4) = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
-        named_bar(1 + grp, 128);
+        named_bar(1, 256);
         if (cs == 0) {
           float sum[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) sum[e] = 0.f;
 #pragma unroll
           for (int c2 = 0; c2 < CS; ++c2) {
-            const float* r2 = sm.red[grp][w4 + c2] + lane * 8;
+            const float* r2 = sm.red[w8 + c2] + lane * 8;
             const float4 a = *reinterpret_cast<const float4*>(r2);
             const float4 bq = *reinterpret_cast<const float4*>(r2 + 4);
             sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
           }
           qk_finish<G>(u, pg, n, j0, sum, s, st, cap, isd);
         }
-        named_bar(1 + grp, 128);
+        named_bar(1, 256);
       }
     }
   }
