@@ -18,6 +18,7 @@
  *   akv_combine           <- (split-K reduction; AttentionResult.o SPEC.md:309-312)
  *   akv_decode_step       <- the whole call stack SURVEY §3(2)
  *   akv_export_planes     <- PlaneTensor plane0/1/2 bytes
+ *   akv_error_histogram   <- analysis.relative_error_histogram SPEC.md:410-418
  *
  * Errors: every call returns AKV_OK or a negative code.  Data-dependent
  * errors (non-finite append, degenerate q) are written to caller-provided
@@ -144,6 +145,13 @@ int akv_decode_step(const akv_store_t* store, const akv_cfg_t* cfg, const akv_st
  * [U][cap][d/2] (byte j = nib[2j] | nib[2j+1]<<4).  which: 0 = K, 1 = V. */
 int akv_export_planes(const akv_store_t* store, int32_t which, uint8_t* plane0, uint8_t* plane1,
                       uint8_t* plane2, void* stream);
+
+/* relative_error_histogram over n device (test, ref) fp32
+ * pairs into counts[6] (int64, device; zeroed by the call): buckets {0},
+ * (0,2^-10), [2^-10,2^-9), [2^-9,2^-8), [2^-8,2^-7), [2^-7,inf).  fp16_round:
+ * round both to the fp16 grid first (A-hist, HB:187-190). */
+int akv_error_histogram(const float* test, const float* ref, int64_t n, int32_t fp16_round, int64_t* counts,
+                        void* stream);
 
 #ifdef __cplusplus
 }

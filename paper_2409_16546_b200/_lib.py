@@ -79,12 +79,15 @@ def lib():
             f.argtypes = [P(AkvStore), P(AkvCfg), P(AkvStep), _i32, _c]
         L.akv_export_planes.restype = _i32
         L.akv_export_planes.argtypes = [P(AkvStore), _i32, _c, _c, _c, _c]
+        L.akv_error_histogram.restype = _i32
+        L.akv_error_histogram.argtypes = [_c, _c, ctypes.c_int64, _i32, _c, _c]
         _lib = L
         return L
 
 
 EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_qk",
-                    "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step", "akv_export_planes")
+                    "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step", "akv_export_planes",
+                    "akv_error_histogram")
 
 
 def check(rc: int, what: str) -> None:

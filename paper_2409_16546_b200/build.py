@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "akv")
 LIB = os.path.join(PKG, "libakv.so")
-SOURCES = ["akv_append.cu", "akv_qk.cu", "akv_select.cu", "akv_pv.cu", "akv_api.cu"]
+SOURCES = ["akv_append.cu", "akv_qk.cu", "akv_select.cu", "akv_pv.cu", "akv_api.cu", "akv_analysis.cu"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
