@@ -202,10 +202,12 @@ def main():
     from paper_2409_16546_b200.synth import generate_batch
     import ctypes
 
+    from paper_2409_16546_b200.shard import shard_for
+
     B, Hkv, g, n, desc = CONFIGS[args.config]
     U, H, d = B * Hkv, B * Hkv * g, 128
-    b0 = rank * B  # weak scaling: this rank's global batch offset
-    units = list(range(b0 * Hkv, (b0 + B) * Hkv))
+    # weak scaling: the job's batch is world*B rows; this rank owns rows [rank*B, (rank+1)*B)
+    units = shard_for(world * B, Hkv, world, rank, "batch").units(Hkv)
     t_gen = time.time()
     K, V, Q = generate_batch(B * world, Hkv, n, d, g, 7, units=units, workers=len(os.sched_getaffinity(0)))
     t_gen = time.time() - t_gen

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
   if (threadIdx.x == 0) {
     for (int i = 0; i < PV_NS; ++i) {
       mbar_init(&sm.full[i], 33);  // expect_tx arrival + 32 cp.async arrivals
-      mbar_init(&sm.empty[i], 4);
+      mbar_init(&sm.empty[i], 8);  // one arrival per consumer warp
     }
     mbar_fence_init();
   }

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
   if (threadIdx.x == 0) {
     for (int i = 0; i < QK_NS; ++i) {
       mbar_init(&sm.full[i], 33);  // expect_tx arrival + 32 cp.async arrivals
-      mbar_init(&sm.empty[i], 4);
+      mbar_init(&sm.empty[i], 8);  // one arrival per consumer warp
     }
     mbar_fence_init();
   }

@@ -1,20 +1,21 @@
 #!/bin/bash
-# One GPU call: smoke, gpu parity tests, bench (with CPU baseline), launch list, ncu full of the hot kernels.
+# One GPU call: smoke, gpu parity tests, bench, launch list, ncu full of the hot kernels.
+# Every step has its own timeout (a protocol bug must not eat the call).
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 nproc > gpurun_out/nproc.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 240 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 tail -3 gpurun_out/smoke.log
-timeout 1200 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+timeout 900 python -m pytest tests -m gpu -q --timeout 150 -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -30 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
 tail -3 gpurun_out/bench.log
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "bench ref rc=$?"
-tail -2 gpurun_out/bench_ref.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+if [ "${FULL:-1}" = "1" ]; then
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_bench.log 2>&1
 echo "launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"qk_kernel|select_kernel|pv_kernel" -c 3 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"qk_kernel|select_kernel|pv_kernel" -c 3 \
   -o gpurun_out/prof_c2 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/prof_bench.log 2>&1
 echo "ncu rc=$?"
+fi
 ls -la gpurun_out
