@@ -97,7 +97,7 @@ typedef struct {
   const uint16_t* q;    /* [U*g][d] fp16 bits (in) */
   float* scores;        /* [U*g][cap] raw scores s_t (QK out) */
   float* probs;         /* [U*g][cap] softmax p_t (may alias scores) */
-  float* page_stats;    /* [U*g][max_pages][2] per-page (max, sum exp) */
+  float* page_stats;    /* [U*g][max_pages*P/32][2] per 32-token chunk (max, sum exp) */
   float* o_est;         /* [U*g][d] */
   int32_t* targets;     /* [U*g][d] rule2 targets (AKV_TARGET_UNKNOWN) */
   uint32_t* sel_bits;   /* [U*g][cap/32] selection bitmap */

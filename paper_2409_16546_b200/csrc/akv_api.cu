@@ -74,7 +74,7 @@ static int64_t carve(akv_step_t* st, uint8_t* ws, int32_t U, int32_t G, int32_t 
     return p;
   };
   uint8_t* scores = take(H * cap * 4);
-  uint8_t* page_stats = take(H * max_pages * 2 * 4);
+  uint8_t* page_stats = take(H * max_pages * (P / 32) * 2 * 4);
   uint8_t* o_est = take(H * D * 4);
   uint8_t* targets = take(H * D * 4);
   uint8_t* sel_bits = take(H * (cap / 32) * 4);

@@ -62,7 +62,7 @@ struct alignas(128) PvSmem {
   uint8_t data[PvShape<G>::NS][VS];
   PvAux<G> aux[PvShape<G>::NS];
   PvMeta meta[PvShape<G>::NS];
-  float red[8][G][D];
+  float red[2][8][G][D];  // per-warp partial outputs, double-buffered (one barrier per page)
   uint64_t full[PvShape<G>::NS], empty[PvShape<G>::NS];
 };
 
@@ -393,15 +393,29 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
     }
   } else {
     const int w8 = warp - 1;
-    for (int kp = 0;; ++kp) {
-      float2 acc[G][4];
-      int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8"
+    int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8" (current unit)
+    int cur_u = -1;
+    auto flush_counts = [&]() {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
+        const int a = warp_sum_i(adj[j][0]), b = warp_sum_i(adj[j][1]), c = warp_sum_i(adj[j][2]);
+        if (lane == 0 && cur_u >= 0) {
+          unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + ((size_t)cur_u * G + j) * 8 + 3);
+          if (a) atomicAdd(ct + 0, (unsigned long long)(long long)a);
+          if (b) atomicAdd(ct + 1, (unsigned long long)(long long)b);
+          if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
+        }
         adj[j][0] = adj[j][1] = adj[j][2] = 0;
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < G; ++j) adj[j][0] = adj[j][1] = adj[j][2] = 0;
+    for (int kp = 0;; ++kp) {
+      float2 acc[G][4];
+#pragma unroll
+      for (int j = 0; j < G; ++j)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) acc[j][kk] = make_float2(0.f, 0.f);
-      }
       int u = 0, pg = 0;
       bool done = false;
 #pragma unroll
@@ -415,14 +429,20 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
         if (hf == 0) {
           u = sm.meta[stage].u;
           pg = sm.meta[stage].pg;
+          if (u != cur_u) {
+            flush_counts();
+            cur_u = u;
+          }
         }
         pv_consume_half<G, TRUNC, EXPORT>(sm, stage, w8, cfg, st, cap, acc, adj);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }
       if (done) break;
-      // partial o of the page: half-warps -> warps (shared) -> page
+      // partial o of the page: half-warps -> warp partial (shared, double-buffered) -> every
+      // warp reduces a 16-channel slice over the 8 partials in a fixed order
       const int half = lane >> 4, cl = lane & 15;
+      float (*red)[G][D] = sm.red[kp & 1];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
 #pragma unroll
@@ -431,33 +451,27 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
           acc[j][kk].y += __shfl_xor_sync(0xFFFFFFFFu, acc[j][kk].y, 16);
         }
         if (half == 0) {
-          float4* dst = reinterpret_cast<float4*>(&sm.red[w8][j][cl * 8]);
+          float4* dst = reinterpret_cast<float4*>(&red[w8][j][cl * 8]);
           dst[0] = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
           dst[1] = make_float4(acc[j][2].x, acc[j][2].y, acc[j][3].x, acc[j][3].y);
         }
-        const int a = warp_sum_i(adj[j][0]), b = warp_sum_i(adj[j][1]), c = warp_sum_i(adj[j][2]);
-        if (lane == 0) {
-          unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + ((size_t)u * G + j) * 8 + 3);
-          if (a) atomicAdd(ct + 0, (unsigned long long)(long long)a);
-          if (b) atomicAdd(ct + 1, (unsigned long long)(long long)b);
-          if (c) atomicAdd(ct + 2, (unsigned long long)(long long)c);
-        }
       }
       named_bar(1, 256);
-      for (int j = w8; j < G; j += 8) {
-        float4 o = *reinterpret_cast<const float4*>(&sm.red[0][j][lane * 4]);
+      for (int i = lane; i < G * 4; i += 32) {
+        const int j = i >> 2, c = w8 * 16 + (i & 3) * 4;
+        float4 o = *reinterpret_cast<const float4*>(&red[0][j][c]);
 #pragma unroll
         for (int w = 1; w < 8; ++w) {  // fixed order
-          const float4 a = *reinterpret_cast<const float4*>(&sm.red[w][j][lane * 4]);
+          const float4 a = *reinterpret_cast<const float4*>(&red[w][j][c]);
           o.x += a.x;
           o.y += a.y;
           o.z += a.z;
           o.w += a.w;
         }
-        *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + lane * 4) = o;
+        *reinterpret_cast<float4*>(st.o_partial + (((size_t)u * G + j) * (cap / P) + pg) * D + c) = o;
       }
-      named_bar(1, 256);
     }
+    flush_counts();
   }
 }
 
@@ -477,6 +491,10 @@ __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t c
   for (; pg < npg; ++pg) acc += part[pg * D];
   st.o[(size_t)h * D + threadIdx.x] = acc;
 }
+
+template <int G>
+constexpr bool pv_smem_fits = sizeof(PvSmem<G>) <= 232448;
+static_assert(pv_smem_fits<1> && pv_smem_fits<2> && pv_smem_fits<4> && pv_smem_fits<8>, "PV shared memory > 227 KB");
 
 template <int G, bool TRUNC, bool EXPORT>
 static void launch_pv_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,

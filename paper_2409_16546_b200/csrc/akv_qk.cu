@@ -86,18 +86,19 @@ struct alignas(16) QkMeta {
 };
 
 template <int G>
-struct alignas(128) QkSmem {
-  uint8_t data[QK_NS][QS];
-  QkMeta<G> meta[QK_NS];
-  QkMeta<G> cache[2];        // producer-private: the current unit's lists (one per half)
-  float red[8][P];           // partial token sums per consumer warp (channel split)
-  uint64_t full[QK_NS], empty[QK_NS];
-};
-
-template <int G>
 struct QkSplit {
   static constexpr int CS = G >= 8 ? 1 : 8 / G;  // ways the channel list is split over the 8 consumer warps
   static constexpr int HW = G >= 8 ? G / 8 : 1;  // heads per consumer warp
+  static constexpr int NRED = CS > 1 ? 2 : 1;    // double-buffered partial sums (one barrier per page)
+};
+
+template <int G>
+struct alignas(128) QkSmem {
+  uint8_t data[QK_NS][QS];
+  QkMeta<G> meta[QK_NS];
+  QkMeta<G> cache[2];                    // producer-private: the current unit's lists (one per half)
+  float red[QkSplit<G>::NRED][8][P];     // partial token sums per consumer warp (channel split)
+  uint64_t full[QK_NS], empty[QK_NS];
 };
 
 __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
@@ -380,37 +381,47 @@ __device__ __forceinline__ void qk_consume_half(const QkSmem<G>& sm, int stage, 
   }
 }
 
-template <int G>
-__device__ __forceinline__ void qk_finish(int u, int pg, int n, int j, const float* sv8, const akv_store_t& s,
-                                          const akv_step_t& st, int cap, float isd) {
+// Scale, store and summarise the scores of T consecutive tokens per lane
+// (tokens tok0 .. tok0+T-1, tok0 = first token of this lane): per 32-token
+// chunk (32/T lanes) the (max, sum exp) pair for the split softmax.
+template <int T>
+__device__ __forceinline__ void qk_finish(const float (&raw)[T], int tok0, int n, float* scores_h, float* stats_h,
+                                          float isd) {
+  constexpr int LPC = 32 / T;  // lanes per 32-token chunk
   const int lane = threadIdx.x & 31;
-  const int tok0 = pg * P + lane * 8;
-  const int nv = min(max(n - tok0, 0), 8);
-  const size_t hh = (size_t)u * G + j;
-  float sv[8];
+  const int nv = min(max(n - tok0, 0), T);
+  float sv[T];
   float m = -INFINITY;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    sv[e] = sv8[e] * isd;
+  for (int e = 0; e < T; ++e) {
+    sv[e] = raw[e] * isd;
     if (e < nv) m = fmaxf(m, sv[e]);
   }
-  m = warp_max(m);
+#pragma unroll
+  for (int o = 1; o < LPC; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
   float l = 0.f;
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
+  for (int e = 0; e < T; ++e)
     if (e < nv) l += expf(sv[e] - m);
-  l = warp_sum(l);
-  float* out = st.scores + hh * cap + tok0;
-  if (nv == 8) {
-    reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-    reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
+#pragma unroll
+  for (int o = 1; o < LPC; o <<= 1) l += __shfl_xor_sync(0xFFFFFFFFu, l, o);
+  float* out = scores_h + tok0;
+  if (nv == T) {
+    if constexpr (T == 1) {
+      out[0] = sv[0];
+    } else if constexpr (T == 2) {
+      *reinterpret_cast<float2*>(out) = make_float2(sv[0], sv[1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < T; e += 4) *reinterpret_cast<float4*>(out + e) = make_float4(sv[e], sv[e + 1], sv[e + 2], sv[e + 3]);
+    }
   } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
+    for (int e = 0; e < T; ++e)
       if (e < nv) out[e] = sv[e];
   }
-  if (lane == 0) {
-    float* ps = st.page_stats + (hh * s.max_pages + pg) * 2;
+  if (lane % LPC == 0 && tok0 < n) {
+    float* ps = stats_h + (tok0 >> 5) * 2;
     ps[0] = m;
     ps[1] = l;
   }
@@ -506,34 +517,53 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }
       if (done) break;
-      if (CS == 1) {
+      const int cap_chunks = s.max_pages * (P / 32);
+      if constexpr (CS == 1) {
 #pragma unroll
-        for (int jj = 0; jj < HW; ++jj) qk_finish<G>(u, pg, n, j0 + jj, acc[jj], s, st, cap, isd);
+        for (int jj = 0; jj < HW; ++jj) {
+          const size_t hh = (size_t)u * G + j0 + jj;
+          qk_finish<8>(acc[jj], pg * P + lane * 8, n, st.scores + hh * cap, st.page_stats + hh * cap_chunks * 2, isd);
+        }
       } else {
-        // channel split: reduce the CS partial sums of each head in a fixed order
-        float* rw = sm.red[w8];
+        // channel split: the CS warps of a head publish their partial sums, then each
+        // reduces its own 256/CS-token slice in a fixed order (deterministic).  The
+        // double buffer makes one barrier per page enough.
+        float* rw = sm.red[kp & 1][w8];
         *reinterpret_cast<float4*>(rw + lane * 8) = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
         *reinterpret_cast<float4*>(rw + lane * 8 + 4) = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
         named_bar(1, 256);
-        if (cs == 0) {
-          float sum[8];
+        constexpr int T = G;  // tokens per lane in the reduction: 256 / CS / 32
+        const int tk = cs * (P / CS) + lane * T;
+        float sum[T];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) sum[e] = 0.f;
+        for (int e = 0; e < T; ++e) sum[e] = 0.f;
 #pragma unroll
-          for (int c2 = 0; c2 < CS; ++c2) {
-            const float* r2 = sm.red[w8 + c2] + lane * 8;
+        for (int c2 = 0; c2 < CS; ++c2) {
+          const float* r2 = sm.red[kp & 1][w8 - cs + c2] + tk;
+          if constexpr (T == 1) {
+            sum[0] += r2[0];
+          } else if constexpr (T == 2) {
+            const float2 a = *reinterpret_cast<const float2*>(r2);
+            sum[0] += a.x;
+            sum[1] += a.y;
+          } else {
             const float4 a = *reinterpret_cast<const float4*>(r2);
-            const float4 bq = *reinterpret_cast<const float4*>(r2 + 4);
-            sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
-            sum[4] += bq.x; sum[5] += bq.y; sum[6] += bq.z; sum[7] += bq.w;
+            sum[0] += a.x;
+            sum[1] += a.y;
+            sum[2] += a.z;
+            sum[3] += a.w;
           }
-          qk_finish<G>(u, pg, n, j0, sum, s, st, cap, isd);
         }
-        named_bar(1, 256);
+        const size_t hh = (size_t)u * G + j0;
+        qk_finish<T>(sum, pg * P + tk, n, st.scores + hh * cap, st.page_stats + hh * cap_chunks * 2, isd);
       }
     }
   }
 }
+
+template <int G>
+constexpr bool qk_smem_fits = sizeof(QkSmem<G>) <= 232448;
+static_assert(qk_smem_fits<1> && qk_smem_fits<2> && qk_smem_fits<4> && qk_smem_fits<8>, "QK shared memory > 227 KB");
 
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,

@@ -49,17 +49,20 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
   const int u = h / G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = s.lengths[u];
-  const int npg = (n + P - 1) / P;
+  const int nch = (n + 31) / 32;  // 32-token chunks with (max, sum exp) from the QK kernel
   __shared__ SelSmem sm;
 
   // 1. global softmax statistics (fixed assignment + butterfly: deterministic)
   if (warp == 0) {
-    const float* ps = st.page_stats + (size_t)h * s.max_pages * 2;
+    const float2* ps = reinterpret_cast<const float2*>(st.page_stats) + (size_t)h * s.max_pages * (P / 32);
     float m = -INFINITY;
-    for (int i = lane; i < npg; i += 32) m = fmaxf(m, ps[2 * i]);
+    for (int i = lane; i < nch; i += 32) m = fmaxf(m, ps[i].x);
     m = warp_max(m);
     float l = 0.f;
-    for (int i = lane; i < npg; i += 32) l += ps[2 * i + 1] * expf(ps[2 * i] - m);
+    for (int i = lane; i < nch; i += 32) {
+      const float2 v = ps[i];
+      l += v.y * expf(v.x - m);
+    }
     l = warp_sum(l);
     if (lane == 0) {
       sm.M = m;
