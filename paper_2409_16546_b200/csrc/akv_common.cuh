@@ -7,6 +7,10 @@
 
 #include "akv.h"
 
+#ifndef AKV_PROBE
+#define AKV_PROBE 0  // measurement-aid builds only (tools/build_probe.sh); 0 in libakv.so
+#endif
+
 namespace akv {
 
 constexpr int D = AKV_HEAD_DIM;
@@ -214,6 +218,30 @@ __device__ __forceinline__ int warp_min_i(int v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
   return v;
+}
+
+// A unit's page-table row held in the producer warp's registers: lane l keeps
+// the pool ids of pages l, l+32, l+64, l+96 (contexts up to 32k tokens; longer
+// ones fall back to a global load).  Loaded one unit ahead so the producers
+// never wait on a dependent global load between stages.
+struct UnitPages {
+  int u, n;
+  int pt[4];
+};
+__device__ __forceinline__ void unit_pages_fetch(UnitPages& f, const akv_store_t& s, int u) {
+  const int lane = threadIdx.x & 31;
+  f.u = u;
+  f.n = s.lengths[u];
+  const int32_t* row = s.page_table + (size_t)u * s.max_pages;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) f.pt[k] = lane + 32 * k < s.max_pages ? row[lane + 32 * k] : 0;
+}
+__device__ __forceinline__ size_t unit_page(const UnitPages& f, const akv_store_t& s, int pg) {
+  const int k = pg >> 5;  // warp-uniform
+  int v = k == 0 ? f.pt[0] : (k == 1 ? f.pt[1] : (k == 2 ? f.pt[2] : f.pt[3]));
+  v = __shfl_sync(0xFFFFFFFFu, v, pg & 31);
+  if (pg >= 128) v = s.page_table[(size_t)f.u * s.max_pages + pg];
+  return (size_t)v;
 }
 
 __device__ __forceinline__ long long status_word(long long code, long long pos) { return (code << 60) | pos; }

@@ -40,7 +40,8 @@ constexpr int VS_MID = HR * D, VS_LOW = HR * D + HR * (D / 2);
 template <int G>
 struct PvShape {
   static constexpr int NS = G >= 4 ? 4 : 6;  // ring stages (half pages; shared memory bound for G >= 4)
-  static constexpr int THREADS = 32 * 9;       // 1 producer + 8 consumer warps
+  static constexpr int PRODUCERS = 2;          // producer warp h fills the half-page stages of half h
+  static constexpr int THREADS = 32 * (PRODUCERS + 8);
 };
 
 template <int G>
@@ -81,6 +82,7 @@ __device__ __forceinline__ void t8_words(uint2 h, uint32_t w[4]) {
 // ----------------------------------------------------------------------------
 struct PvPage {
   int u, n;
+  size_t pid;       // pool page id
   uint32_t um, ul;  // lane w < 8: union need words w of the page
 };
 
@@ -149,20 +151,27 @@ __device__ void pv_stage(PvSmem<G>& sm, int stage, int hf, int item, int pg, con
     mt.un_mid[lane] = a;
     mt.un_low[lane] = b;
   }
-  const uint8_t* src = page_ptr(s.v_pool, s.page_table, s.max_pages, f.u, pg);
+  const uint8_t* src = s.v_pool + f.pid * PAGE;
   uint8_t* dst = sm.data[stage];
   PvAux<G>& ax = sm.aux[stage];
   __syncwarp();
+#if AKV_PROBE == 2  // measurement aid: no plane loads (consumer-bound time)
+  if (lane == 0) {
+    mbar_arrive(&sm.full[stage]);
+#else
   if (lane == 0) {
     // head rows of this half: one TMA bulk copy
     mbar_arrive_expect_tx(&sm.full[stage], (uint32_t)rows * D);
     if (rows) bulk_g2s(dst, src + hf * HR * D, (uint32_t)rows * D, &sm.full[stage]);
+#endif
     const uint32_t vbytes = (uint32_t)rows * D + (uint32_t)(nm + nl) * (D / 2);
     atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)f.u * 4 + 1), (unsigned long long)vbytes);
   }
   // nibble rows (64 B) and per-row metadata: cp.async from all lanes
+#if AKV_PROBE != 2
   cp_rows<4, D / 2>(um, dst + VS_MID, src + MID + hf * HR * (D / 2));
   cp_rows<4, D / 2>(ul, dst + VS_LOW, src + LOW + hf * HR * (D / 2));
+#endif
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     const size_t h = (size_t)f.u * G + j;
@@ -353,18 +362,27 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
   const long long total = (long long)s.n_units * npg_max;
   const bool uniform = cfg.force_tier != 0 || TRUNC;
 
-  if (warp == 0) {
+  if (warp < PvShape<G>::PRODUCERS) {
+    const int my_hf = warp;  // both producers walk the same pages; producer h stages half h
     // ---------------- producer: contiguous item range, need bits one page ahead ----------------
     const long long per = (total + gridDim.x - 1) / gridDim.x;
     const long long i0 = (long long)blockIdx.x * per, i1 = min(total, i0 + per);
     int k = 0;
     PvPage cur, nxt;
+    UnitPages up_cur, up_nxt;  // page-table rows: the current unit and (prefetched) the next
+    up_cur.u = -1;
+    if (i0 < i1) unit_pages_fetch(up_nxt, s, (int)(i0 / npg_max));
     auto advance = [&](long long from, PvPage& f) -> long long {
       for (long long idx = from; idx < i1; ++idx) {
         const int u = (int)(idx / npg_max), pg = (int)(idx % npg_max);
-        const int n = s.lengths[u];
+        if (u != up_cur.u) {
+          up_cur = up_nxt;
+          if ((long long)(u + 1) * npg_max < i1) unit_pages_fetch(up_nxt, s, u + 1);
+        }
+        const int n = up_cur.n;
         if (pg * P >= n) continue;
         pv_fetch<G>(f, cfg, st, u, pg, n, cap, uniform);
+        f.pid = unit_page(up_cur, s, pg);
         return idx;
       }
       return -1;
@@ -375,16 +393,16 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
       cur = nxt;
       nidx = advance(idx + 1, nxt);  // prefetch the next page's need bits
       const int pg = (int)(idx % npg_max);
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf, ++k) {
-        const int stage = k % PV_NS;
-        mbar_wait(&sm.empty[stage], ((k / PV_NS) & 1) ^ 1);
-        pv_stage<G>(sm, stage, hf, (int)idx, pg, cur, s, st, cap);
+      {
+        const int kk = k + my_hf, stage = kk % PV_NS;
+        mbar_wait(&sm.empty[stage], ((kk / PV_NS) & 1) ^ 1);
+        pv_stage<G>(sm, stage, my_hf, (int)idx, pg, cur, s, st, cap);
+        k += 2;
       }
     }
-    for (int t = 0; t < 2; ++t, ++k) {
-      const int stage = k % PV_NS;
-      mbar_wait(&sm.empty[stage], ((k / PV_NS) & 1) ^ 1);
+    {
+      const int kk = k + my_hf, stage = kk % PV_NS;
+      mbar_wait(&sm.empty[stage], ((kk / PV_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
       __syncwarp();
       mbar_arrive(&sm.full[stage]);                 // 32 lane arrivals ...
@@ -392,7 +410,7 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
       __syncwarp();
     }
   } else {
-    const int w8 = warp - 1;
+    const int w8 = warp - PvShape<G>::PRODUCERS;
     int adj[G][3];  // element-count adjustments relative to "every valid unselected row is T8" (current unit)
     int cur_u = -1;
     auto flush_counts = [&]() {
@@ -434,7 +452,9 @@ __global__ void __launch_bounds__(PvShape<G>::THREADS, 1) pv_kernel(akv_store_t 
             cur_u = u;
           }
         }
+#if AKV_PROBE != 1  // measurement aid: 1 = no consumer compute (load-bound time)
         pv_consume_half<G, TRUNC, EXPORT>(sm, stage, w8, cfg, st, cap, acc, adj);
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }

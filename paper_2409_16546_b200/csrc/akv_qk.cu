@@ -35,8 +35,18 @@
 
 namespace akv {
 
+#if AKV_PROBE == 3  // measurement aid: cycle accounting of the ring (tools/build_probe.sh)
+__device__ unsigned long long qk_prof[16];
+#define QK_T0(v) const long long v = clock64()
+#define QK_ACC(var, t0) var += clock64() - (t0)
+#else
+#define QK_T0(v)
+#define QK_ACC(var, t0)
+#endif
+
 constexpr int QK_NS = 6;                 // ring stages (half pages)
-constexpr int QK_THREADS = 32 * 9;       // 1 producer + 8 consumer warps
+constexpr int QK_PRODUCERS = 2;          // producer warp h fills the half-page stages of half h
+constexpr int QK_THREADS = 32 * (QK_PRODUCERS + 8);  // 2 producer + 8 consumer warps
 constexpr int HCH = D / 2;               // channels per half page
 constexpr int QS = HCH * P * 2;          // 32 KB stage: head [64][256] | mid [64][128] | low [64][128]
 constexpr int QS_MID = HCH * P, QS_LOW = HCH * P + HCH * (P / 2);
@@ -111,7 +121,7 @@ __device__ __forceinline__ uint32_t ent_of(const uint4& e, int i) {
 // ----------------------------------------------------------------------------
 template <int G>
 struct QkUnit {
-  int u, n;
+  UnitPages pages;
   uint32_t cm[4];
   uint32_t qw[G][4];
 };
@@ -120,8 +130,7 @@ struct QkUnit {
 template <int G>
 __device__ __forceinline__ void qk_fetch_unit(QkUnit<G>& f, const akv_store_t& s, const akv_step_t& st, int u) {
   const int lane = threadIdx.x & 31;
-  f.u = u;
-  f.n = s.lengths[u];
+  unit_pages_fetch(f.pages, s, u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) f.cm[k] = s.colmax[(size_t)u * D + lane + 32 * k];
 #pragma unroll
@@ -135,7 +144,7 @@ __device__ __forceinline__ void qk_fetch_unit(QkUnit<G>& f, const akv_store_t& s
 // and writes the per-step bookkeeping (K tiers, K counters, status, bytes).
 // Lane l owns channels l + 32k (k = 0..3): words k = 0, 1 are half 0.
 template <int G, bool TRUNC>
-__device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, const akv_cfg_t& cfg,
+__device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, int my_hf, const akv_cfg_t& cfg,
                                  const akv_step_t& st, uint32_t (&bm)[4], uint32_t (&bl)[4]) {
   const int lane = threadIdx.x & 31;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
@@ -175,7 +184,7 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
       ucode[k] = max(ucode[k], cd);
     }
     if (book) {  // per-step bookkeeping, once per unit
-      const size_t h = (size_t)f.u * G + j;
+      const size_t h = (size_t)f.pages.u * G + j;
       int c8 = 0, c12 = 0, c16 = 0, bad = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -187,9 +196,9 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
       }
       if (lane == 0) {
         int64_t* ct = st.counters + h * 8;
-        ct[0] = (int64_t)c8 * f.n;
-        ct[1] = (int64_t)c12 * f.n;
-        ct[2] = (int64_t)c16 * f.n;
+        ct[0] = (int64_t)c8 * f.pages.n;
+        ct[1] = (int64_t)c12 * f.pages.n;
+        ct[2] = (int64_t)c16 * f.pages.n;
         ct[3] = ct[4] = ct[5] = ct[6] = ct[7] = 0;
         long long w = 0;
         if (bad) w = status_word(AKV_STATUS_BAD_Q, 0);
@@ -212,6 +221,7 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
   }
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
+    if (hf != my_hf) continue;  // each producer builds only its own half's list
     QkMeta<G>& mt = sm.cache[hf];
     const int n8 = __popc(b8[2 * hf]) + __popc(b8[2 * hf + 1]);
     const int nm = __popc(bm[2 * hf]) + __popc(bm[2 * hf + 1]);
@@ -262,8 +272,8 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
     }
   }
   if (book && lane == 0) {
-    st.unit_bytes[(size_t)f.u * 4 + 0] = (int64_t)f.n * nh + (int64_t)(f.n / 2) * (nm_all + nl_all);
-    st.unit_bytes[(size_t)f.u * 4 + 1] = 0;
+    st.unit_bytes[(size_t)f.pages.u * 4 + 0] = (int64_t)f.pages.n * nh + (int64_t)(f.pages.n / 2) * (nm_all + nl_all);
+    st.unit_bytes[(size_t)f.pages.u * 4 + 1] = 0;
   }
   __syncwarp();
 }
@@ -271,9 +281,10 @@ __device__ void qk_unit_prologue(QkSmem<G>& sm, const QkUnit<G>& f, bool book, c
 // Publish one half page into a ring stage: the cached half list + item fields,
 // then the copies (head half by TMA bulk copy; needed mid / low rows by cp.async).
 template <int G>
-__device__ void qk_stage(QkSmem<G>& sm, int stage, int hf, int item, int u, int pg, int n, const akv_store_t& s,
+__device__ void qk_stage(QkSmem<G>& sm, int stage, int hf, int item, int u, int pg, int n, const uint8_t* src,
                          const uint32_t (&bm)[4], const uint32_t (&bl)[4]) {
   const int lane = threadIdx.x & 31;
+  QK_T0(t_a);
   QkMeta<G>& mt = sm.meta[stage];
   constexpr int W = sizeof(QkMeta<G>) / 16;
   const uint4* srcm = reinterpret_cast<const uint4*>(&sm.cache[hf]);
@@ -286,18 +297,39 @@ __device__ void qk_stage(QkSmem<G>& sm, int stage, int hf, int item, int u, int 
     mt.pg = pg;
     mt.n = n;
   }
-  const uint8_t* src = page_ptr(s.k_pool, s.page_table, s.max_pages, u, pg);
   uint8_t* dst = sm.data[stage];
   __syncwarp();
+#if AKV_PROBE == 3
+  long long t_b = clock64();
+  if (lane == 0) atomicAdd(&qk_prof[11], (unsigned long long)(t_b - t_a));
+#endif
+#if AKV_PROBE == 2  // measurement aid: no plane loads (consumer-bound time)
+  if (lane == 0) mbar_arrive(&sm.full[stage]);
+#else
   if (lane == 0) {
     mbar_arrive_expect_tx(&sm.full[stage], HCH * P);
     bulk_g2s(dst, src + hf * HCH * P, HCH * P, &sm.full[stage]);
   }
-  const uint32_t mm[2] = {bm[2 * hf], bm[2 * hf + 1]};
-  const uint32_t ml[2] = {bl[2 * hf], bl[2 * hf + 1]};
+#if AKV_PROBE == 3
+  __syncwarp();
+  long long t_c = clock64();
+  if (lane == 0) atomicAdd(&qk_prof[8], (unsigned long long)(t_c - t_b));
+#endif
+  const uint32_t mm[2] = {hf ? bm[2] : bm[0], hf ? bm[3] : bm[1]};
+  const uint32_t ml[2] = {hf ? bl[2] : bl[0], hf ? bl[3] : bl[1]};
   cp_rows<2, P / 2>(mm, dst + QS_MID, src + MID + hf * HCH * (P / 2));
   cp_rows<2, P / 2>(ml, dst + QS_LOW, src + LOW + hf * HCH * (P / 2));
+#endif
+#if AKV_PROBE == 3
+  __syncwarp();
+  long long t_d = clock64();
+  if (lane == 0) atomicAdd(&qk_prof[9], (unsigned long long)(t_d - t_c));
+#endif
   cp_async_arrive_noinc(&sm.full[stage]);
+#if AKV_PROBE == 3
+  __syncwarp();
+  if (lane == 0) atomicAdd(&qk_prof[10], (unsigned long long)(clock64() - t_d));
+#endif
 }
 
 // ----------------------------------------------------------------------------
@@ -444,10 +476,16 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
   __syncthreads();
   const long long total = (long long)s.n_units * npg_max;
 
-  if (warp == 0) {
-    // ---------------- producer: contiguous item range, Rule 1 once per unit ----------------
+  if (warp < QK_PRODUCERS) {
+    // ---------------- producers: contiguous item range, Rule 1 once per unit ----------------
+    // Both producers walk the same items; producer h fills the stages of half h.
+    const int my_hf = warp;
     const long long per = (total + gridDim.x - 1) / gridDim.x;
     const long long i0 = (long long)blockIdx.x * per, i1 = min(total, i0 + per);
+#if AKV_PROBE == 3
+    long long p_wait = 0, p_issue = 0;
+    const long long p_start = clock64();
+#endif
     QkUnit<G> cur, nxt;
     uint32_t bm[4] = {0, 0, 0, 0}, bl[4] = {0, 0, 0, 0};
     int cur_u = -1;
@@ -459,20 +497,32 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
         cur = nxt;
         if ((long long)(u + 1) * npg_max < i1) qk_fetch_unit<G>(nxt, s, st, u + 1);  // prefetch the next unit
         cur_u = u;
-        if (cur.n > 0) qk_unit_prologue<G, TRUNC>(sm, cur, pg == 0, cfg, st, bm, bl);
+        if (cur.pages.n > 0) qk_unit_prologue<G, TRUNC>(sm, cur, pg == 0 && my_hf == 0, my_hf, cfg, st, bm, bl);
       }
-      if (pg * P >= cur.n) continue;  // beyond this unit's length (ragged batch)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf, ++k) {
-        const int stage = k % QK_NS;
-        mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
-        qk_stage<G>(sm, stage, hf, (int)idx, u, pg, cur.n, s, bm, bl);
+      if (pg * P >= cur.pages.n) continue;  // beyond this unit's length (ragged batch)
+      const uint8_t* src = s.k_pool + unit_page(cur.pages, s, pg) * PAGE;
+      {
+        const int kk = k + my_hf, stage = kk % QK_NS;
+        QK_T0(tw);
+        mbar_wait(&sm.empty[stage], ((kk / QK_NS) & 1) ^ 1);
+        QK_ACC(p_wait, tw);
+        QK_T0(ti);
+        qk_stage<G>(sm, stage, my_hf, (int)idx, u, pg, cur.pages.n, src, bm, bl);
+        QK_ACC(p_issue, ti);
+        k += 2;
       }
     }
-    // terminator: the next page slot (both halves)
-    for (int t = 0; t < 2; ++t, ++k) {
-      const int stage = k % QK_NS;
-      mbar_wait(&sm.empty[stage], ((k / QK_NS) & 1) ^ 1);
+#if AKV_PROBE == 3
+    if (lane == 0) {
+      atomicAdd(&qk_prof[0], (unsigned long long)p_wait);
+      atomicAdd(&qk_prof[1], (unsigned long long)p_issue);
+      atomicAdd(&qk_prof[2], (unsigned long long)(clock64() - p_start));
+    }
+#endif
+    // terminator: this producer's half of the next page slot
+    {
+      const int kk = k + my_hf, stage = kk % QK_NS;
+      mbar_wait(&sm.empty[stage], ((kk / QK_NS) & 1) ^ 1);
       if (lane == 0) sm.meta[stage].item = -1;
       __syncwarp();
       mbar_arrive(&sm.full[stage]);                 // 32 lane arrivals ...
@@ -481,7 +531,7 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
     }
   } else {
     // ---------------- consumers: eight warps share each page ----------------
-    const int w8 = warp - 1;
+    const int w8 = warp - QK_PRODUCERS;
     uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
     if (TRUNC) {
       const int kb = cfg.trunc_bits - 6;
@@ -491,6 +541,10 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
       tf = fill | (fill << 16);
     }
     const int cs = w8 % CS, j0 = (w8 / CS) * HW;
+#if AKV_PROBE == 3
+    long long c_wait = 0, c_comp = 0;
+    const long long c_start = clock64();
+#endif
     for (int kp = 0;; ++kp) {
       float acc[HW][8];
 #pragma unroll
@@ -502,7 +556,9 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int kk = 2 * kp + hf, stage = kk % QK_NS;
+        QK_T0(cw);
         mbar_wait(&sm.full[stage], (kk / QK_NS) & 1);
+        QK_ACC(c_wait, cw);
         if (sm.meta[stage].item < 0) {
           done = true;
           break;
@@ -512,11 +568,25 @@ __global__ void __launch_bounds__(QK_THREADS, 1) qk_kernel(akv_store_t s, akv_cf
           pg = sm.meta[stage].pg;
           n = sm.meta[stage].n;
         }
+#if AKV_PROBE != 1  // measurement aid: 1 = no consumer compute (load-bound time)
+        QK_T0(cc);
         qk_consume_half<G, TRUNC>(sm, stage, w8, acc, tkm, tf);
+        QK_ACC(c_comp, cc);
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);  // stage no longer read by this warp
       }
-      if (done) break;
+      if (done) {
+#if AKV_PROBE == 3
+        if (lane == 0) {
+          atomicAdd(&qk_prof[3], (unsigned long long)c_wait);
+          atomicAdd(&qk_prof[4], (unsigned long long)c_comp);
+          atomicAdd(&qk_prof[5], (unsigned long long)(clock64() - c_start));
+          
+        }
+#endif
+        break;
+      }
       const int cap_chunks = s.max_pages * (P / 32);
       if constexpr (CS == 1) {
 #pragma unroll
@@ -595,3 +665,12 @@ void launch_qk(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st,
 }
 
 }  // namespace akv
+
+#if AKV_PROBE == 3
+extern "C" int akv_probe_read_qk(unsigned long long* host) {
+  cudaMemcpyFromSymbol(host, akv::qk_prof, sizeof(akv::qk_prof));
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(akv::qk_prof, z, sizeof(z));
+  return 0;
+}
+#endif
