@@ -88,6 +88,13 @@ __device__ __forceinline__ uint2 ld_stream_u64(const void* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ uint4 ld_stream_u128(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const void* p, uint64_t pol) {
   uint32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));

@@ -1,0 +1,462 @@
+// scores_aligned for every (unit, q-head) of a batch.
+//
+// Direct-load streaming kernel: every warp owns a contiguous range of
+// (unit, page) items (balanced split over all resident warps; no shared-memory
+// staging, no cross-warp synchronisation).  Per item the warp
+//
+//  1. (once per unit) evaluates Rule 1 for the unit's q-heads
+//     (rule1_target SPEC.md:157-165, required_mantissa_bits :139-147,
+//     tier_for_bits :148-156, k_channel_tiers :175-183, SURVEY App. A
+//     A-K/D1/D2/D8) and builds its channel list in shared memory ordered by
+//     union class: T8 channels first (head plane only), then T12/T16
+//     channels; SKIP channels are dropped (0 bits read).  The warp that owns
+//     a unit's page 0 writes the per-step bookkeeping (K tiers, K counters,
+//     status, plane bytes);
+//  2. streams the page, half-warp per channel row, lane = 16 consecutive
+//     tokens: one LDG.128 covers two listed channels' 256 B head-plane rows;
+//     only T12/T16 channels add an LDG.64 of their 128 B mid row (+ the low
+//     row for T16).  The lists are padded per class to 8 channels so every
+//     batch is homogeneous (no per-channel branches).  Loads run two batches
+//     of 8 channels ahead of the math, straight into registers (L1
+//     no-allocate, L2 evict-first);
+//  3. rebuilds fp16 words with PRMT/LOP3 (midpoint fill for absent nibbles,
+//     HB:160-179) and accumulates q_c * K~ with the mixed-precision FHFMA
+//     (exact fp16 x fp16 products, fp32 sums, D9);
+//  4. scales by 1/sqrt(d) after accumulation and writes the
+//     page's scores plus a (max, sum exp) pair per 32-token chunk for the
+//     split softmax.
+// Each page's result is independent of which warp computes it: deterministic.
+#include <algorithm>
+
+#include "akv_common.cuh"
+
+namespace akv {
+
+constexpr int QK_WARPS = 4;  // warps per CTA
+
+template <int G>
+struct QkShape {
+  // resident CTAs per SM (register budget: 64K / (128 threads * MINB))
+  static constexpr int HG = G < 4 ? G : 4;          // q-heads per pass over a page (accumulator budget)
+  static constexpr int MINB = G == 1 ? 3 : 2;
+};
+
+template <int E, int Q>
+__device__ __forceinline__ float fma_hh(uint32_t a, uint32_t qpair, float c) {
+  float d;
+  if (E == 0 && Q == 0)
+    asm("{\n\t.reg .f16 a0, a1, q0, q1;\n\tmov.b32 {a0, a1}, %1;\n\tmov.b32 {q0, q1}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a0, q0, %3;\n\t}"
+        : "=f"(d) : "r"(a), "r"(qpair), "f"(c));
+  else if (E == 1 && Q == 0)
+    asm("{\n\t.reg .f16 a0, a1, q0, q1;\n\tmov.b32 {a0, a1}, %1;\n\tmov.b32 {q0, q1}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a1, q0, %3;\n\t}"
+        : "=f"(d) : "r"(a), "r"(qpair), "f"(c));
+  else if (E == 0 && Q == 1)
+    asm("{\n\t.reg .f16 a0, a1, q0, q1;\n\tmov.b32 {a0, a1}, %1;\n\tmov.b32 {q0, q1}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a0, q1, %3;\n\t}"
+        : "=f"(d) : "r"(a), "r"(qpair), "f"(c));
+  else
+    asm("{\n\t.reg .f16 a0, a1, q0, q1;\n\tmov.b32 {a0, a1}, %1;\n\tmov.b32 {q0, q1}, %2;\n\t"
+        "fma.rn.f32.f16 %0, a1, q1, %3;\n\t}"
+        : "=f"(d) : "r"(a), "r"(qpair), "f"(c));
+  return d;
+}
+
+template <int Q>
+__device__ __forceinline__ void fma8(const uint32_t w[4], uint32_t qpair, float acc[8]) {
+  acc[0] = fma_hh<0, Q>(w[0], qpair, acc[0]);
+  acc[1] = fma_hh<1, Q>(w[0], qpair, acc[1]);
+  acc[2] = fma_hh<0, Q>(w[1], qpair, acc[2]);
+  acc[3] = fma_hh<1, Q>(w[1], qpair, acc[3]);
+  acc[4] = fma_hh<0, Q>(w[2], qpair, acc[4]);
+  acc[5] = fma_hh<1, Q>(w[2], qpair, acc[5]);
+  acc[6] = fma_hh<0, Q>(w[3], qpair, acc[6]);
+  acc[7] = fma_hh<1, Q>(w[3], qpair, acc[7]);
+}
+
+// Per-warp unit state in shared memory.  List positions: T8 class in
+// [0, n8p), T12/T16 class in [n8p, nlist), each padded to a multiple of 8 with
+// copies of the class's first channel (q = 0: adds nothing, row already in
+// flight).  Batch b = positions 8b..8b+7; lane (half h, i) handles position
+// 8b + 2i + h.  Per-lane arrays are stored at slot 8b + 4h + i so one LDS.128
+// fetches a lane's four values of a batch.
+template <int G>
+struct alignas(16) QkWarp {
+  uint32_t off[D + 16];                 // slot -> channel * P
+  uint32_t qrep[G][D + 16];             // slot -> q | q << 16 (fp16), 0 for SKIP heads / pads
+  uint2 hm[G > 1 ? G : 1][D + 16];      // slot -> per-head (keep, fill) word masks (T12/T16 class, G > 1)
+  uint32_t low[(D + 16) / 32 + 1];      // slot bitmask: T16 (low row needed)
+  int n8p, nlist, unit, pad;
+};
+
+__device__ __forceinline__ int qk_slot(int pos) { return (pos & ~7) | ((pos & 1) << 2) | ((pos >> 1) & 3); }
+
+struct KBatch {
+  uint4 h[4];
+  uint2 m[4], l[4];
+};
+
+template <int G>
+__device__ __forceinline__ void k_load(KBatch& X, const QkWarp<G>& ws, int b, bool full, const uint8_t* base,
+                                       int l16, int half, uint64_t pol) {
+  const uint4 o = *reinterpret_cast<const uint4*>(&ws.off[8 * b + 4 * half]);
+  const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+  const uint32_t lowm = (ws.low[(8 * b) >> 5] >> ((8 * b + 4 * half) & 31)) & 0xFu;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    X.h[i] = ld_stream_u128(base + ov[i] + l16 * 16, pol);
+    if (full) {
+      const uint8_t* mrow = base + MID + (ov[i] >> 1) + l16 * 8;
+      X.m[i] = ld_stream_u64(mrow, pol);
+      X.l[i] = make_uint2(0x88888888u, 0x88888888u);
+      if ((lowm >> i) & 1u) X.l[i] = ld_stream_u64(mrow + (LOW - MID), pol);
+    }
+  }
+}
+
+template <int HG, bool FULL, bool TRUNC, int G>
+__device__ __forceinline__ void k_compute(const KBatch& X, const QkWarp<G>& ws, int b, int half, int j0,
+                                          float (&acc)[HG][16], uint32_t tkm, uint32_t tf) {
+  const int sl = 8 * b + 4 * half;
+  uint32_t qv[HG][4];
+#pragma unroll
+  for (int jj = 0; jj < HG; ++jj) {
+    const uint4 q = *reinterpret_cast<const uint4*>(&ws.qrep[j0 + jj][sl]);
+    qv[jj][0] = q.x;
+    qv[jj][1] = q.y;
+    qv[jj][2] = q.z;
+    qv[jj][3] = q.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t w[8];  // 16 tokens as half2 words
+    if (FULL) {
+      assemble8(X.h[i].x, X.h[i].y, X.m[i].x, X.l[i].x, w);
+      assemble8(X.h[i].z, X.h[i].w, X.m[i].y, X.l[i].y, w + 4);
+    } else {
+      const uint32_t c80 = 0x80808080u;
+      const uint32_t hv[4] = {X.h[i].x, X.h[i].y, X.h[i].z, X.h[i].w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        w[2 * r] = prmt(hv[r], c80, 0x1404);
+        w[2 * r + 1] = prmt(hv[r], c80, 0x3424);
+      }
+    }
+    if (TRUNC) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = (w[k] & tkm) | tf;
+    }
+#pragma unroll
+    for (int jj = 0; jj < HG; ++jj) {
+      uint32_t wj[8];
+      if (G > 1 && FULL) {
+        const uint2 hm = ws.hm[j0 + jj][sl + i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wj[k] = (w[k] & hm.x) | hm.y;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wj[k] = w[k];
+      }
+      fma8<0>(wj, qv[jj][i], acc[jj]);
+      fma8<0>(wj + 4, qv[jj][i], acc[jj] + 8);
+    }
+  }
+}
+
+// Rule 1 for unit u, all G heads; builds the warp's channel lists.
+// Lane l owns channels l + 32k (k = 0..3).
+template <int G, bool TRUNC>
+__device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int u,
+                           int n, bool book) {
+  const int lane = threadIdx.x & 31;
+  const bool aligned = cfg.force_tier == 0 && !TRUNC;
+  uint32_t cm[4], qw[G][4];
+  int code[G][4], ucode[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) cm[k] = s.colmax[(size_t)u * D + lane + 32 * k] & 0x7FFFu;
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qw[j][k] = st.q[((size_t)u * G + j) * D + lane + 32 * k];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    int pe[4], mx = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool valid = (qw[j][k] & 0x7FFFu) && cm[k] && finite16(qw[j][k]);
+      pe[k] = valid ? magexp16(qw[j][k]) + magexp16(cm[k]) + 1 : INT_MIN;
+      mx = max(mx, pe[k]);
+    }
+    const int maxpe = warp_max_i(mx);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int cd;
+      if (!aligned) {
+        cd = TRUNC ? 16 : cfg.force_tier;
+      } else if (maxpe == INT_MIN) {
+        cd = 16;  // degenerate: status reported below, output undefined
+      } else {
+        const int t = min(max(pe[k] - maxpe + 9 + cfg.margin_bits, 0), 10);  // pe - u - 1 + margin, u = maxpe - 10
+        cd = t <= 2 ? 8 : (t <= 6 ? 12 : 16);
+        const bool qz = (qw[j][k] & 0x7FFFu) == 0, cz = cm[k] == 0;
+        if (cfg.zero_skip) {
+          if (qz || cz) cd = 0;
+        } else if (qz) {
+          cd = 8;  // D1
+        } else if (cz) {
+          cd = 16;  // D2
+        }
+      }
+      code[j][k] = cd;
+      ucode[k] = max(ucode[k], cd);
+    }
+    if (book) {  // per-step bookkeeping, once per unit (the page-0 item)
+      const size_t h = (size_t)u * G + j;
+      int c8 = 0, c12 = 0, c16 = 0, bad = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        st.k_tiers[h * D + lane + 32 * k] = (uint8_t)code[j][k];
+        c8 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 8));
+        c12 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 12));
+        c16 += __popc(__ballot_sync(0xFFFFFFFFu, code[j][k] == 16));
+        bad += __popc(__ballot_sync(0xFFFFFFFFu, !finite16(qw[j][k])));
+      }
+      if (lane == 0) {
+        int64_t* ct = st.counters + h * 8;
+        ct[0] = (int64_t)c8 * n;
+        ct[1] = (int64_t)c12 * n;
+        ct[2] = (int64_t)c16 * n;
+        ct[3] = ct[4] = ct[5] = ct[6] = ct[7] = 0;
+        long long w = 0;
+        if (bad) w = status_word(AKV_STATUS_BAD_Q, 0);
+        else if (aligned && maxpe == INT_MIN) w = status_word(AKV_STATUS_DEGENERATE, 0);
+        st.status[h] = w;
+      }
+    }
+  }
+  // lists: T8 class first, then T12/T16 (ascending channel inside each class)
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t b8[4], bf[4], b16[4];
+  int n8 = 0, nf = 0, n16 = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    b8[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 8);
+    bf[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
+    b16[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 16);
+    n8 += __popc(b8[k]);
+    nf += __popc(bf[k]);
+    n16 += __popc(b16[k]);
+  }
+  const int n8p = (n8 + 7) & ~7, nlp = n8p + ((nf + 7) & ~7);
+  for (int i = lane; i < (D + 16) / 32 + 1; i += 32) ws.low[i] = 0u;
+  __syncwarp();
+  int base8 = 0, basef = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = lane + 32 * k;
+    int pos = -1;
+    if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
+    else if (ucode[k] >= 12) pos = n8p + basef + __popc(bf[k] & lt);
+    if (pos >= 0) {
+      const int sl = qk_slot(pos);
+      ws.off[sl] = (uint32_t)c * P;
+      if (ucode[k] == 16) atomicOr(&ws.low[sl >> 5], 1u << (sl & 31));
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const uint32_t qh = code[j][k] ? (qw[j][k] & 0xFFFFu) : 0u;
+        ws.qrep[j][sl] = qh | (qh << 16);
+        if (G > 1) {
+          const int cd = code[j][k];
+          ws.hm[j][sl] = cd >= 16 ? make_uint2(0xFFFFFFFFu, 0u)
+                                  : (cd == 12 ? make_uint2(0xFFF0FFF0u, 0x00080008u) : make_uint2(0xFF00FF00u, 0x00800080u));
+        }
+      }
+    }
+    base8 += __popc(b8[k]);
+    basef += __popc(bf[k]);
+  }
+  __syncwarp();
+  // pads: copies of the class's first channel (row already in flight) with q = 0
+  const uint32_t off8 = n8 ? ws.off[qk_slot(0)] : 0u, offf = nf ? ws.off[qk_slot(n8p)] : 0u;
+  const bool low_f = nf ? ((ws.low[qk_slot(n8p) >> 5] >> (qk_slot(n8p) & 31)) & 1u) : false;
+  __syncwarp();
+  for (int pos = lane; pos < nlp; pos += 32) {
+    const bool pad = pos < n8p ? pos >= n8 : pos >= n8p + nf;
+    if (!pad) continue;
+    const int sl = qk_slot(pos);
+    ws.off[sl] = pos < n8p ? off8 : offf;
+    if (pos >= n8p && low_f) atomicOr(&ws.low[sl >> 5], 1u << (sl & 31));
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      ws.qrep[j][sl] = 0u;
+      if (G > 1) ws.hm[j][sl] = make_uint2(0xFFFFFFFFu, 0u);
+    }
+  }
+  if (book && lane == 0) {
+    st.unit_bytes[(size_t)u * 4 + 0] = (int64_t)n * (n8 + nf) + (int64_t)(n / 2) * (nf + n16);
+    st.unit_bytes[(size_t)u * 4 + 1] = 0;
+  }
+  if (lane == 0) {
+    ws.n8p = n8p;
+    ws.nlist = nlp;
+    ws.unit = u;
+  }
+  __syncwarp();
+}
+
+// Scale, store and summarise one page's scores.  After the half-warp fold
+// every lane holds the totals of tokens 16*l16 .. +15; lane (half h) finishes
+// tokens 16*l16 + 8h .. +7.  A 32-token chunk = lanes {2c, 2c+1} x both halves.
+__device__ __forceinline__ void qk_finish(const float* raw, int tok0, int n, float* scores_h, float* stats_h,
+                                          float isd) {
+  const int lane = threadIdx.x & 31;
+  const int nv = min(max(n - tok0, 0), 8);
+  float sv[8];
+  float m = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    sv[e] = raw[e] * isd;
+    if (e < nv) m = fmaxf(m, sv[e]);
+  }
+  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));
+  float l = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (e < nv) l += expf(sv[e] - m);
+  l += __shfl_xor_sync(0xFFFFFFFFu, l, 1);
+  l += __shfl_xor_sync(0xFFFFFFFFu, l, 16);
+  float* out = scores_h + tok0;
+  if (nv == 8) {
+    reinterpret_cast<float4*>(out)[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+    reinterpret_cast<float4*>(out)[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < nv) out[e] = sv[e];
+  }
+  if ((lane & 17) == 0 && tok0 < n) {  // lanes 2c of half 0 own chunk c
+    float* ps = stats_h + (tok0 >> 5) * 2;
+    ps[0] = m;
+    ps[1] = l;
+  }
+}
+
+template <int G, bool TRUNC>
+__global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv_store_t s, akv_cfg_t cfg,
+                                                                             akv_step_t st, int cap, float isd,
+                                                                             int npg_max) {
+  constexpr int HG = QkShape<G>::HG;
+  extern __shared__ __align__(16) uint8_t qk_smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, l16 = lane & 15;
+  QkWarp<G>& ws = reinterpret_cast<QkWarp<G>*>(qk_smem_raw)[warp];
+  if (lane == 0) ws.unit = -1;
+  __syncwarp();
+  const uint64_t pol = evict_first_policy();
+  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
+  if (TRUNC) {
+    const int kb = cfg.trunc_bits - 6;
+    const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
+    const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
+    tkm = km | (km << 16);
+    tf = fill | (fill << 16);
+  }
+  // balanced contiguous item range of this warp
+  const long long total = (long long)s.n_units * npg_max;
+  const long long nw = (long long)gridDim.x * QK_WARPS, gw = (long long)blockIdx.x * QK_WARPS + warp;
+  const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
+  const int cap_chunks = s.max_pages * (P / 32);
+  UnitPages up;
+  up.u = -1;
+  up.n = 0;
+
+  for (long long item = i0; item < i1; ++item) {
+    const int u = (int)(item / npg_max), pg = (int)(item % npg_max);
+    if (u != up.u) unit_pages_fetch(up, s, u);
+    const int n = up.n;
+    if (pg * P >= n) continue;
+    if (ws.unit != u || pg == 0) k_prologue<G, TRUNC>(ws, s, cfg, st, u, n, pg == 0);
+    const uint8_t* base = s.k_pool + unit_page(up, s, pg) * PAGE;
+    const int nb8 = ws.n8p >> 3, nb = ws.nlist >> 3;
+
+#pragma unroll 1
+    for (int j0 = 0; j0 < G; j0 += HG) {
+      float acc[HG][16];
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[jj][e] = 0.f;
+
+      // software pipeline over homogeneous batches (T8 batches, then T12/T16
+      // batches): the next two batches are in flight while one is computed
+      KBatch X[3];
+      auto load = [&](int b, KBatch& B) { k_load<G>(B, ws, b, b >= nb8, base, l16, half, pol); };
+      auto comp = [&](int b, const KBatch& B) {
+        if (b < nb8) k_compute<HG, false, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);
+        else k_compute<HG, true, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);
+      };
+      if (nb > 0) load(0, X[0]);
+      if (nb > 1) load(1, X[1]);
+      int b = 0;
+      for (; b + 3 <= nb; b += 3) {
+        load(b + 2, X[2]);
+        comp(b, X[0]);
+        if (b + 3 < nb) load(b + 3, X[0]);
+        comp(b + 1, X[1]);
+        if (b + 4 < nb) load(b + 4, X[1]);
+        comp(b + 2, X[2]);
+      }
+      if (b < nb) comp(b, X[0]);
+      if (b + 1 < nb) comp(b + 1, X[1]);
+
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        float mine[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {  // fold the two half-warps; keep this lane's 8 tokens
+          const float lo = acc[jj][e] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e], 16);
+          const float hi = acc[jj][e + 8] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e + 8], 16);
+          mine[e] = half ? hi : lo;
+        }
+        const size_t hh = (size_t)u * G + j0 + jj;
+        qk_finish(mine, pg * P + 16 * l16 + 8 * half, n, st.scores + hh * cap, st.page_stats + hh * cap_chunks * 2,
+                  isd);
+      }
+    }
+  }
+}
+
+template <int G, bool TRUNC>
+static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
+                        cudaStream_t stream) {
+  static int resident = 0;
+  const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(qk_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk_kernel<G, TRUNC>, 32 * QK_WARPS, smem);
+    resident = sms * std::max(per, 1);
+  }
+  const int cap = s.max_pages * P;
+  const int npg = (max_len + P - 1) / P;
+  const long long items = (long long)s.n_units * npg;
+  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + QK_WARPS - 1) / QK_WARPS, 1));
+  const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
+  qk_kernel<G, TRUNC><<<grid, 32 * QK_WARPS, smem, stream>>>(s, cfg, st, cap, isd, npg);
+}
+
+void launch_qk(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len, cudaStream_t stream) {
+  const bool tr = cfg.trunc_bits != 0;
+  switch (cfg.group) {
+    case 1: tr ? launch_qk_t<1, true>(s, cfg, st, max_len, stream) : launch_qk_t<1, false>(s, cfg, st, max_len, stream); break;
+    case 2: tr ? launch_qk_t<2, true>(s, cfg, st, max_len, stream) : launch_qk_t<2, false>(s, cfg, st, max_len, stream); break;
+    case 4: tr ? launch_qk_t<4, true>(s, cfg, st, max_len, stream) : launch_qk_t<4, false>(s, cfg, st, max_len, stream); break;
+    case 8: tr ? launch_qk_t<8, true>(s, cfg, st, max_len, stream) : launch_qk_t<8, false>(s, cfg, st, max_len, stream); break;
+  }
+}
+
+}  // namespace akv
