@@ -389,6 +389,269 @@ __global__ void __launch_bounds__(32 * PV_WARPS, UNIFORM ? 2 : PvShape<G>::MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// pv v3: per-warp TMA ring.  Every warp streams its own (unit, page, head-pass)
+// items through a private NS-slot shared-memory ring: lane 0 issues one
+// cp.async.bulk per 64-row stage of head rows (8 KB; uniform tiers add the
+// stage's mid / low rows) plus the stage's p_t and selection words, completing
+// on the slot's mbarrier; the warp computes from shared memory with the same
+// row code as the register-pipelined kernel.  In-flight data lives in shared
+// memory (NS-1 stages ahead), not registers.
+// ---------------------------------------------------------------------------
+template <int G, bool UNIFORM>
+struct Pv3Shape {
+  static constexpr int HG = G < 4 ? G : 4;
+  static constexpr int NPASS = G / HG;
+  static constexpr int ROWS = UNIFORM ? 32 : 64;                 // rows per stage
+  static constexpr int HEAD = ROWS * D;                          // head bytes per stage
+  static constexpr int NIB = UNIFORM ? ROWS * (D / 2) : 0;       // mid (= low) bytes per stage
+  static constexpr int SLOT = HEAD + 2 * NIB;                    // 8 KB
+  // per-page metadata (issued with the page's first stage): p[HG][P], sel[HG][8], need[G][2][8]
+  static constexpr int M_P = 0, M_SEL = HG * P * 4, M_NEED = M_SEL + HG * 32;
+  static constexpr int META = M_NEED + G * 64;
+  static constexpr int NS = 2;      // stages per warp ring (one in flight while one is computed)
+  static constexpr int WARPS = 4;
+  static constexpr int PER_WARP = NS * SLOT + 2 * META + NS * 8;
+  static constexpr int SMEM = WARPS * PER_WARP;
+  static constexpr int MINB = G == 1 ? 3 : 2;
+};
+
+struct PvCursor {
+  long long item;     // (unit * npg + page) * npass + pass
+  int sub;            // stage within the page
+  int u, pg, pass, rows, nsub, npage;  // npage: pages started by this cursor (meta buffer parity)
+  size_t pid;
+  UnitPages up;
+};
+
+template <int ROWS>
+__device__ __forceinline__ bool pv_cursor_seek(PvCursor& c, long long i1, const akv_store_t& s, int npg_max,
+                                               int npass) {
+  for (; c.item < i1; ++c.item) {
+    const long long pi = c.item / npass;
+    const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
+    if (u != c.up.u) unit_pages_fetch(c.up, s, u);
+    if (pg * P >= c.up.n) continue;
+    c.u = u;
+    c.pg = pg;
+    c.pass = (int)(c.item % npass);
+    c.rows = min(c.up.n - pg * P, P);
+    c.nsub = (c.rows + ROWS - 1) / ROWS;
+    c.sub = 0;
+    c.pid = unit_page(c.up, s, pg);
+    ++c.npage;
+    return true;
+  }
+  return false;
+}
+
+template <int ROWS>
+__device__ __forceinline__ bool pv_cursor_next(PvCursor& c, long long i1, const akv_store_t& s, int npg_max,
+                                               int npass) {
+  if (c.sub + 1 < c.nsub) {
+    ++c.sub;
+    return true;
+  }
+  ++c.item;
+  return pv_cursor_seek<ROWS>(c, i1, s, npg_max, npass);
+}
+
+template <int G, bool UNIFORM>
+__device__ __forceinline__ void pv3_issue(uint8_t* slot, uint8_t* meta, uint64_t* bar, const PvCursor& c,
+                                          const akv_store_t& s, const akv_step_t& st, int cap) {
+  using S = Pv3Shape<G, UNIFORM>;
+  const uint8_t* vb = s.v_pool + c.pid * PAGE;
+  const int r0 = c.sub * S::ROWS;
+  const int capw = cap >> 5;
+  const bool first = c.sub == 0;
+  const uint32_t mbytes = first ? S::HG * P * 4 + (UNIFORM ? 0 : S::HG * 32 + G * 64) : 0;
+  mbar_arrive_expect_tx(bar, S::SLOT + mbytes);
+  bulk_g2s(slot, vb + r0 * D, S::HEAD, bar);
+  if (UNIFORM) {
+    bulk_g2s(slot + S::HEAD, vb + MID + r0 * (D / 2), S::NIB, bar);
+    bulk_g2s(slot + S::HEAD + S::NIB, vb + LOW + r0 * (D / 2), S::NIB, bar);
+  }
+  if (first) {
+#pragma unroll
+    for (int jj = 0; jj < S::HG; ++jj) {
+      const size_t h = (size_t)c.u * G + c.pass * S::HG + jj;
+      bulk_g2s(meta + S::M_P + jj * P * 4, st.probs + h * cap + (size_t)c.pg * P, P * 4, bar);
+      if (!UNIFORM) bulk_g2s(meta + S::M_SEL + jj * 32, st.sel_bits + h * capw + c.pg * 8, 32, bar);
+    }
+    if (!UNIFORM) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const uint32_t* nb = st.need_bits + ((size_t)c.u * G + j) * 2 * capw + c.pg * 8;
+        bulk_g2s(meta + S::M_NEED + j * 64, nb, 32, bar);
+        bulk_g2s(meta + S::M_NEED + j * 64 + 32, nb + capw, 32, bar);
+      }
+    }
+  }
+}
+
+template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
+__global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, UNIFORM>::MINB)
+    pv3_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, int npg_max) {
+  using S = Pv3Shape<G, UNIFORM>;
+  constexpr int HG = S::HG, NS = S::NS;
+  extern __shared__ __align__(128) uint8_t pv3_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 3, cg = lane & 7;
+  uint8_t* ring = pv3_smem + warp * S::PER_WARP;
+  uint8_t* metab = ring + NS * S::SLOT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(metab + 2 * S::META);
+  if (lane == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  constexpr bool aligned = !UNIFORM;
+  const int uni = TRUNC ? 16 : cfg.force_tier;
+  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
+  if (TRUNC) {
+    const int kb = cfg.trunc_bits - 6;
+    const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
+    const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
+    tkm = km | (km << 16);
+    tf = fill | (fill << 16);
+  }
+  const long long total = (long long)s.n_units * npg_max * S::NPASS;
+  const long long nw = (long long)gridDim.x * S::WARPS, gw = (long long)blockIdx.x * S::WARPS + warp;
+  const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
+
+  PvCursor ic, cc;  // issue / consume cursors
+  ic.item = i0;
+  ic.up.u = -1;
+  ic.up.n = 0;
+  ic.npage = 0;
+  bool iv = pv_cursor_seek<S::ROWS>(ic, i1, s, npg_max, S::NPASS);
+  cc = ic;
+  bool cv = iv;
+  int kiss = 0;
+  for (; kiss < NS - 1 && iv; ++kiss) {
+    if (lane == 0)
+      pv3_issue<G, UNIFORM>(ring + (kiss % NS) * S::SLOT, metab + (ic.npage & 1) * S::META, &full[kiss % NS], ic, s,
+                            st, cap);
+    iv = pv_cursor_next<S::ROWS>(ic, i1, s, npg_max, S::NPASS);
+  }
+
+  float2 acc[HG][8];
+  int adj[HG][3], base[HG];
+  PvCtx c;
+  for (int k = 0; cv; ++k) {
+    // keep NS-1 stages ahead: the slot being refilled was consumed at k-1 by this warp
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (iv) {
+      if (lane == 0)
+        pv3_issue<G, UNIFORM>(ring + (kiss % NS) * S::SLOT, metab + (ic.npage & 1) * S::META, &full[kiss % NS], ic,
+                              s, st, cap);
+      ++kiss;
+      iv = pv_cursor_next<S::ROWS>(ic, i1, s, npg_max, S::NPASS);
+    }
+    const int slot = k % NS;
+    mbar_wait(&full[slot], (k / NS) & 1);
+    const uint8_t* sd = ring + slot * S::SLOT;
+    const uint8_t* md = metab + (cc.npage & 1) * S::META;
+    const int j0 = cc.pass * HG;
+    if (cc.sub == 0) {
+      // page start: accumulators, fetch plan (union need words of every q-head) from the page metadata
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        adj[jj][0] = adj[jj][1] = adj[jj][2] = 0;
+        base[jj] = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[jj][q] = make_float2(0.f, 0.f);
+      }
+      c.vb = s.v_pool + cc.pid * PAGE;
+      c.rows = cc.rows;
+      c.pg = cc.pg;
+      c.u = cc.u;
+      c.cap = cap;
+      uint32_t w = 0u;
+      if (lane < 16) {
+        const int chk = lane & 7;
+        const int valid = min(max(c.rows - 32 * chk, 0), 32);
+        const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+        if (!aligned) {
+          w = (lane < 8 ? uni >= 12 : uni >= 16) ? vm : 0u;
+        } else {
+          const uint32_t* nw8 = reinterpret_cast<const uint32_t*>(md + S::M_NEED);
+#pragma unroll
+          for (int j = 0; j < G; ++j) w |= nw8[j * 16 + (lane >> 3) * 8 + chk];
+          w &= vm;
+        }
+      }
+      c.nwu = w;
+      if (cc.pass == 0) {
+        const int nib = warp_sum_i(__popc(w));
+        if (lane == 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)cc.u * 4 + 1),
+                    (unsigned long long)c.rows * D + (unsigned long long)nib * (D / 2));
+      }
+    }
+    const float* sp = reinterpret_cast<const float*>(md + S::M_P);
+    const uint32_t* ss = reinterpret_cast<const uint32_t*>(md + S::M_SEL);
+#pragma unroll
+    for (int bb = 0; bb < S::ROWS / 16; ++bb) {
+      const int b = cc.sub * (S::ROWS / 16) + bb;  // 16-row batch index inside the page
+      if (16 * b >= c.rows) break;
+      VBatch<HG, UNIFORM> X;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rl = 16 * bb + 4 * i + r4;  // row inside the stage
+        const bool valid = 16 * b + 4 * i + r4 < c.rows;
+        X.h[i] = valid ? *reinterpret_cast<const uint4*>(sd + rl * D + cg * 16) : make_uint4(0u, 0u, 0u, 0u);
+        if (UNIFORM) {
+          X.m[i] = valid ? *reinterpret_cast<const uint2*>(sd + S::HEAD + rl * (D / 2) + cg * 8) : make_uint2(0u, 0u);
+          X.l[i] = valid ? *reinterpret_cast<const uint2*>(sd + S::HEAD + S::NIB + rl * (D / 2) + cg * 8)
+                         : make_uint2(0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        const int row = 16 * b + (lane & 15);
+        X.p[jj] = (lane < 16 && row < c.rows) ? sp[jj * P + row] : 0.f;
+        X.sel[jj] = UNIFORM ? 0u : ss[jj * 8 + (b >> 1)];
+      }
+      v_compute<G, HG, TRUNC, EXPORT, UNIFORM>(X, c, b, j0, cfg, st, acc, adj, base, tkm, tf);
+    }
+    if (cc.sub + 1 == cc.nsub) {
+      // page end: fold the four row groups, lanes 0..7 write 16 channels each; element counts
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc[jj][q].x += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][q].x, 8);
+          acc[jj][q].y += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][q].y, 8);
+          acc[jj][q].x += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][q].x, 16);
+          acc[jj][q].y += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][q].y, 16);
+        }
+        const size_t h = (size_t)cc.u * G + j0 + jj;
+        if (r4 == 0) {
+          float4* dst = reinterpret_cast<float4*>(st.o_partial + (h * (cap / P) + cc.pg) * D + cg * 16);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            dst[q4] = make_float4(acc[jj][2 * q4].x, acc[jj][2 * q4].y, acc[jj][2 * q4 + 1].x, acc[jj][2 * q4 + 1].y);
+        }
+        const int a = warp_sum_i(adj[jj][0]), b1 = warp_sum_i(adj[jj][1]), c2 = warp_sum_i(adj[jj][2]);
+        if (lane == 0) {
+          unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + h * 8 + 3);
+          long long t8 = a, t12 = b1, t16 = c2;
+          const long long bs = (long long)base[jj] * D;
+          if (aligned || uni == 8) t8 += bs;
+          else if (uni == 12) t12 += bs;
+          else t16 += bs;
+          if (t8) atomicAdd(ct + 0, (unsigned long long)t8);
+          if (t12) atomicAdd(ct + 1, (unsigned long long)t12);
+          if (t16) atomicAdd(ct + 2, (unsigned long long)t16);
+        }
+      }
+    }
+    cv = pv_cursor_next<S::ROWS>(cc, i1, s, npg_max, S::NPASS);
+  }
+}
+
 // o = o_est + sum over the unit's pages of o_partial, fixed order (deterministic).
 __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st) {
   const int h = blockIdx.x;
@@ -406,9 +669,37 @@ __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t c
   st.o[(size_t)h * D + threadIdx.x] = acc;
 }
 
+#ifndef AKV_PV_V3
+#define AKV_PV_V3 1
+#endif
+
+template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
+static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
+                         cudaStream_t stream) {
+  using S = Pv3Shape<G, UNIFORM>;
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, 32 * S::WARPS, S::SMEM);
+    resident = sms * std::max(per, 1);
+  }
+  const int cap = s.max_pages * P;
+  const int npg = (max_len + P - 1) / P;
+  const long long items = (long long)s.n_units * npg * S::NPASS;
+  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  pv3_kernel<G, TRUNC, EXPORT, UNIFORM><<<grid, 32 * S::WARPS, S::SMEM, stream>>>(s, cfg, st, cap, npg);
+}
+
 template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
 static void launch_pv_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
+  if (AKV_PV_V3) {
+    launch_pv3_t<G, TRUNC, EXPORT, UNIFORM>(s, cfg, st, max_len, stream);
+    return;
+  }
   static int resident = 0;
   if (!resident) {
     int dev = 0, sms = 0, per = 0;

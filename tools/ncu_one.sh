@@ -1,6 +1,12 @@
 #!/bin/bash
-# ncu --set full of the first launch of kernels matching $1 (one bench step)
+# ncu (speed-of-light, memory, warp state, source counters) of kernels matching $1 in one bench step;
+# exports raw metrics + SASS source counters as CSV (the .ncu-rep embeds the whole module and is too big to ship back)
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$1" -c ${2:-1} \
-  -o gpurun_out/prof_${3:-one} python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/prof_${3:-one}.log 2>&1
+tag=${3:-one}
+timeout 600 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section WarpStateStats --section SourceCounters \
+  --section LaunchStats --section Occupancy --clock-control none -k regex:"$1" -c ${2:-1} \
+  -o /tmp/prof_$tag python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/prof_$tag.log 2>&1
 echo "ncu rc=$?"
+ncu -i /tmp/prof_$tag.ncu-rep --page raw --csv > gpurun_out/prof_${tag}_raw.csv 2>&1
+ncu -i /tmp/prof_$tag.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_${tag}_sass.csv 2>&1
+ls -la gpurun_out/
