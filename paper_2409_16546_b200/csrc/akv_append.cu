@@ -10,6 +10,8 @@ namespace akv {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const uint16_t* __restrict__ k,
                                                          const uint16_t* __restrict__ v, int64_t* status) {
+  pdl_trigger();
+  pdl_wait();
   const int u = blockIdx.x;
   const int c = threadIdx.x;
   const uint32_t kw = k[(size_t)u * D + c];
@@ -209,7 +211,7 @@ extern "C" int akv_append(const akv_store_t* store, const uint16_t* k, const uin
   if (n_new == 0 || store->n_units == 0) return AKV_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_new == 1) {
-    append_token_kernel<<<store->n_units, D, 0, st>>>(*store, k, v, status);
+    launch_pdl(append_token_kernel, dim3(store->n_units), dim3(D), 0, st, *store, k, v, status);
   } else {
     append_validate_kernel<<<store->n_units, 256, 0, st>>>(*store, k, v, n_new, status);
     const int chunks = (n_new + P - 1) / P + 1;

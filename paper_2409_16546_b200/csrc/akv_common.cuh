@@ -251,6 +251,29 @@ __device__ __forceinline__ size_t unit_page(const UnitPages& f, const akv_store_
   return (size_t)v;
 }
 
+// Programmatic dependent launch (PDL): every step kernel is launched with
+// programmatic stream serialization, lets its dependent start launching at
+// once, and waits for its predecessor's memory before touching any of it, so
+// launch latency overlaps the previous kernel's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kernel, args...);
+}
+
 __device__ __forceinline__ long long status_word(long long code, long long pos) { return (code << 60) | pos; }
 
 __device__ __forceinline__ const uint8_t* page_ptr(const uint8_t* pool, const int32_t* table, int max_pages, int u,

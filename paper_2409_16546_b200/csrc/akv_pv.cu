@@ -1,46 +1,37 @@
 // output_aligned for every (unit, q-head).
 //
-// Direct-load streaming kernel: every warp owns a contiguous range of
-// (unit, page) items (balanced split over all resident warps; no shared-memory
-// staging, no cross-warp synchronisation).  Lane = (row r4 = lane / 8,
-// 16-channel group cg = lane % 8): one LDG.128 reads four V head-plane rows
-// (4 x 128 B, token-major) of a page; a batch is 16 rows.  Per batch the warp
-// also loads the rows' p_t (lanes 0..15) and the selection word, and the
-// 64 B mid / low nibble rows only of rows whose "need mid / need low" bit
-// (akv_softmax_select's RowMax superset rule, OR-ed over the
-// kv-head's q-heads) is set.  Loads run two batches ahead of the math,
-// straight into registers (L1 no-allocate, L2 evict-first).
+// Per-warp TMA ring: every warp owns a balanced contiguous range of
+// (unit, page, head-pass) items and streams them through a private 2-slot
+// shared-memory ring.  Lane 0 issues one cp.async.bulk per 64-row stage of V
+// head rows (8 KB, token-major; uniform tiers: 32 rows + their mid / low rows)
+// and, with a page's first stage, the page's p_t, selection words and the
+// q-heads' need-mid / need-low words (akv_softmax_select's RowMax superset
+// rule); everything completes on the slot's mbarrier.  The warp
+// computes one stage while the next is in flight; no cross-warp sync.
+// Lane = (row r4 = lane / 8, 16-channel group cg = lane % 8): one LDS.128
+// reads four rows; a batch is 16 rows.
 //
-// A batch with no row needing a nibble (the common case) takes the
+// A batch with no row in the union fetch plan (the common case) takes the
 // branch-free path: T8 words by PRMT (midpoint fill, HB:160-179), fp16 ->
 // fp32 by HADD2.F32, p_t * V~ by the packed FFMA2 into fp32.
 // Selected rows carry p = 0 here (D6: their T16 contribution is o_est).
-// Other rows apply each q-head's rule: p_t = 0 -> T8 (D5); ELEMENT: keep mid
-// iff max(bexp,1) + e(p_t) > 17 + target_r - margin, low iff > that + 4 (D4);
-// row strategy: the row tier (D7); forced / baseline tiers.  Truncation is
-// applied after the fetch, so the masks equal the oracle's bit for bit.
-// The page's partial output goes to o_partial[h][page]; akv_combine adds o_est
-// and the partials in a fixed order (deterministic).
+// Other rows fetch the needed 64 B nibble rows (LDG) and apply each q-head's
+// rule: p_t = 0 -> T8 (D5); ELEMENT: keep mid iff max(bexp,1) + e(p_t) >
+// 17 + target_r - margin, low iff > that + 4 (D4); row strategy: the row tier
+// (D7); forced / baseline tiers.  Truncation is applied after the fetch, so
+// the masks equal the oracle's bit for bit.  The page's partial output goes to
+// o_partial[h][page]; akv_combine adds o_est and the partials in a fixed order
+// (deterministic).
 #include <algorithm>
 
 #include "akv_common.cuh"
 
 namespace akv {
 
-constexpr int PV_WARPS = 4;  // warps per CTA
-
-template <int G>
-struct PvShape {
-  static constexpr int HG = G < 4 ? G : 4;  // q-heads per pass over a page (accumulator budget)
-#ifndef AKV_PV_MINB1
-#define AKV_PV_MINB1 3
-#endif
-  static constexpr int MINB = G == 1 ? AKV_PV_MINB1 : 2;
-};
-
-// Aligned mode keeps only the head rows in flight (nibble rows are rare and are
+// One 16-row batch as the row code sees it (filled from the stage in shared
+// memory).  Aligned mode stages only head rows (nibble rows are rare and are
 // fetched on demand by the generic path); uniform tiers (forced / baseline)
-// keep the nibble rows in the pipeline too.
+// stage the nibble rows too.
 template <int HG, bool NIB>
 struct VBatch {
   uint4 h[4];                        // head bytes: row 16b + 4i + r4, channels 16cg .. +15
@@ -65,37 +56,6 @@ struct PvCtx {
   int pg, u, cap;
   uint32_t nwu;       // lanes 0..7: union need-mid word of chunk lane; lanes 8..15: need-low word of chunk lane-8
 };
-
-template <int G, int HG, bool UNIFORM>
-__device__ __forceinline__ void v_load(VBatch<HG, UNIFORM>& X, const PvCtx& c, int b, int j0, const akv_step_t& st,
-                                       uint64_t pol) {
-  const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
-  const int ch = b >> 1;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = 16 * b + 4 * i + r4;
-    X.h[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (UNIFORM) {
-      X.m[i] = make_uint2(0u, 0u);
-      X.l[i] = make_uint2(0u, 0u);
-    }
-    if (row < c.rows) {
-      X.h[i] = ld_stream_u128(c.vb + row * D + cg * 16, pol);
-      if (UNIFORM) {
-        X.m[i] = ld_stream_u64(c.vb + MID + row * (D / 2) + cg * 8, pol);
-        X.l[i] = ld_stream_u64(c.vb + LOW + row * (D / 2) + cg * 8, pol);
-      }
-    }
-  }
-  const int prow = 16 * b + (lane & 15);
-  const int capw = c.cap >> 5;
-#pragma unroll
-  for (int jj = 0; jj < HG; ++jj) {
-    const size_t h = (size_t)c.u * G + j0 + jj;
-    X.p[jj] = (lane < 16 && prow < c.rows) ? st.probs[h * c.cap + (size_t)c.pg * P + prow] : 0.f;
-    X.sel[jj] = UNIFORM ? 0u : st.sel_bits[h * capw + c.pg * 8 + ch];
-  }
-}
 
 template <int G, int HG, bool TRUNC, bool EXPORT, bool UNIFORM>
 __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const PvCtx& c, int b, int j0, const akv_cfg_t& cfg,
@@ -264,131 +224,6 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
   }
 }
 
-template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
-__global__ void __launch_bounds__(32 * PV_WARPS, UNIFORM ? 2 : PvShape<G>::MINB) pv_kernel(akv_store_t s, akv_cfg_t cfg,
-                                                                             akv_step_t st, int cap, int npg_max) {
-  constexpr int HG = PvShape<G>::HG;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r4 = lane >> 3, cg = lane & 7;
-  const uint64_t pol = evict_first_policy();
-  constexpr bool aligned = !UNIFORM;
-  const int uni = TRUNC ? 16 : cfg.force_tier;
-  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
-  if (TRUNC) {
-    const int kb = cfg.trunc_bits - 6;
-    const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
-    const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
-    tkm = km | (km << 16);
-    tf = fill | (fill << 16);
-  }
-  const int capw = cap >> 5;
-  const long long total = (long long)s.n_units * npg_max;
-  const long long nw = (long long)gridDim.x * PV_WARPS, gw = (long long)blockIdx.x * PV_WARPS + warp;
-  const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
-  UnitPages up;
-  up.u = -1;
-  up.n = 0;
-
-  for (long long item = i0; item < i1; ++item) {
-    const int u = (int)(item / npg_max), pg = (int)(item % npg_max);
-    if (u != up.u) unit_pages_fetch(up, s, u);
-    const int n = up.n;
-    if (pg * P >= n) continue;
-    PvCtx c;
-    c.vb = s.v_pool + unit_page(up, s, pg) * PAGE;
-    c.rows = min(n - pg * P, P);
-    c.pg = pg;
-    c.u = u;
-    c.cap = cap;
-    // union over the kv-head's q-heads of the page's need words (fetch plan), valid rows only
-    {
-      uint32_t w = 0u;
-      if (lane < 16) {
-        const int chk = lane & 7;
-        const int valid = min(max(c.rows - 32 * chk, 0), 32);
-        const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
-        if (!aligned) {
-          w = (lane < 8 ? uni >= 12 : uni >= 16) ? vm : 0u;
-        } else {
-#pragma unroll
-          for (int j = 0; j < G; ++j)
-            w |= st.need_bits[((size_t)u * G + j) * 2 * capw + (lane >> 3) * capw + pg * 8 + chk];
-          w &= vm;
-        }
-      }
-      c.nwu = w;
-      const int nib = warp_sum_i(__popc(w));
-      if (lane == 0)
-        atomicAdd(reinterpret_cast<unsigned long long*>(st.unit_bytes + (size_t)u * 4 + 1),
-                  (unsigned long long)c.rows * D + (unsigned long long)nib * (D / 2));
-    }
-    const int nb = (c.rows + 15) >> 4;
-
-#pragma unroll 1
-    for (int j0 = 0; j0 < G; j0 += HG) {
-      float2 acc[HG][8];
-      int adj[HG][3], base[HG];
-#pragma unroll
-      for (int jj = 0; jj < HG; ++jj) {
-        adj[jj][0] = adj[jj][1] = adj[jj][2] = 0;
-        base[jj] = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[jj][k] = make_float2(0.f, 0.f);
-      }
-      VBatch<HG, UNIFORM> X[3];
-      auto load = [&](int b, VBatch<HG, UNIFORM>& B) { v_load<G, HG, UNIFORM>(B, c, b, j0, st, pol); };
-      auto comp = [&](int b, const VBatch<HG, UNIFORM>& B) {
-        v_compute<G, HG, TRUNC, EXPORT, UNIFORM>(B, c, b, j0, cfg, st, acc, adj, base, tkm, tf);
-      };
-      if (nb > 0) load(0, X[0]);
-      if (nb > 1) load(1, X[1]);
-      int b = 0;
-      for (; b + 3 <= nb; b += 3) {
-        load(b + 2, X[2]);
-        comp(b, X[0]);
-        if (b + 3 < nb) load(b + 3, X[0]);
-        comp(b + 1, X[1]);
-        if (b + 4 < nb) load(b + 4, X[1]);
-        comp(b + 2, X[2]);
-      }
-      if (b < nb) comp(b, X[0]);
-      if (b + 1 < nb) comp(b + 1, X[1]);
-
-      // page partial: fold the four row groups, lanes 0..7 write 16 channels each
-#pragma unroll
-      for (int jj = 0; jj < HG; ++jj) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          acc[jj][k].x += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][k].x, 8);
-          acc[jj][k].y += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][k].y, 8);
-          acc[jj][k].x += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][k].x, 16);
-          acc[jj][k].y += __shfl_xor_sync(0xFFFFFFFFu, acc[jj][k].y, 16);
-        }
-        const size_t h = (size_t)u * G + j0 + jj;
-        if (r4 == 0) {
-          float4* dst = reinterpret_cast<float4*>(st.o_partial + (h * (cap / P) + pg) * D + cg * 16);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            dst[q4] = make_float4(acc[jj][2 * q4].x, acc[jj][2 * q4].y, acc[jj][2 * q4 + 1].x, acc[jj][2 * q4 + 1].y);
-        }
-        // element counts: base rows at T8 (aligned) or the uniform tier, plus the generic-path moves
-        const int a = warp_sum_i(adj[jj][0]), b1 = warp_sum_i(adj[jj][1]), c2 = warp_sum_i(adj[jj][2]);
-        if (lane == 0) {
-          unsigned long long* ct = reinterpret_cast<unsigned long long*>(st.counters + h * 8 + 3);
-          long long t8 = a, t12 = b1, t16 = c2;
-          const long long bs = (long long)base[jj] * D;
-          if (aligned || uni == 8) t8 += bs;
-          else if (uni == 12) t12 += bs;
-          else t16 += bs;
-          if (t8) atomicAdd(ct + 0, (unsigned long long)t8);
-          if (t12) atomicAdd(ct + 1, (unsigned long long)t12);
-          if (t16) atomicAdd(ct + 2, (unsigned long long)t16);
-        }
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // pv v3: per-warp TMA ring.  Every warp streams its own (unit, page, head-pass)
 // items through a private NS-slot shared-memory ring: lane 0 issues one
@@ -505,6 +340,8 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
     mbar_fence_init();
   }
   __syncwarp();
+  pdl_trigger();
+  pdl_wait();
   constexpr bool aligned = !UNIFORM;
   const int uni = TRUNC ? 16 : cfg.force_tier;
   uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
@@ -654,6 +491,8 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
 
 // o = o_est + sum over the unit's pages of o_partial, fixed order (deterministic).
 __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st) {
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x;
   const int u = h / cfg.group;
   const int n = s.lengths[u];
@@ -668,10 +507,6 @@ __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t c
   for (; pg < npg; ++pg) acc += part[pg * D];
   st.o[(size_t)h * D + threadIdx.x] = acc;
 }
-
-#ifndef AKV_PV_V3
-#define AKV_PV_V3 1
-#endif
 
 template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
 static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
@@ -690,29 +525,7 @@ static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg * S::NPASS;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
-  pv3_kernel<G, TRUNC, EXPORT, UNIFORM><<<grid, 32 * S::WARPS, S::SMEM, stream>>>(s, cfg, st, cap, npg);
-}
-
-template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
-static void launch_pv_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
-                        cudaStream_t stream) {
-  if (AKV_PV_V3) {
-    launch_pv3_t<G, TRUNC, EXPORT, UNIFORM>(s, cfg, st, max_len, stream);
-    return;
-  }
-  static int resident = 0;
-  if (!resident) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pv_kernel<G, TRUNC, EXPORT, UNIFORM>, 32 * PV_WARPS, 0);
-    resident = sms * std::max(per, 1);
-  }
-  const int cap = s.max_pages * P;
-  const int npg = (max_len + P - 1) / P;
-  const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + PV_WARPS - 1) / PV_WARPS, 1));
-  pv_kernel<G, TRUNC, EXPORT, UNIFORM><<<grid, 32 * PV_WARPS, 0, stream>>>(s, cfg, st, cap, npg);
+  launch_pdl(pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg);
 }
 
 template <int G>
@@ -720,14 +533,14 @@ static void launch_pv_g(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
                         cudaStream_t stream) {
   const bool ex = st.v_tiers != nullptr;
   if (cfg.trunc_bits) {
-    if (ex) launch_pv_t<G, true, true, true>(s, cfg, st, max_len, stream);
-    else launch_pv_t<G, true, false, true>(s, cfg, st, max_len, stream);
+    if (ex) launch_pv3_t<G, true, true, true>(s, cfg, st, max_len, stream);
+    else launch_pv3_t<G, true, false, true>(s, cfg, st, max_len, stream);
   } else if (cfg.force_tier) {
-    if (ex) launch_pv_t<G, false, true, true>(s, cfg, st, max_len, stream);
-    else launch_pv_t<G, false, false, true>(s, cfg, st, max_len, stream);
+    if (ex) launch_pv3_t<G, false, true, true>(s, cfg, st, max_len, stream);
+    else launch_pv3_t<G, false, false, true>(s, cfg, st, max_len, stream);
   } else {
-    if (ex) launch_pv_t<G, false, true, false>(s, cfg, st, max_len, stream);
-    else launch_pv_t<G, false, false, false>(s, cfg, st, max_len, stream);
+    if (ex) launch_pv3_t<G, false, true, false>(s, cfg, st, max_len, stream);
+    else launch_pv3_t<G, false, false, false>(s, cfg, st, max_len, stream);
   }
 }
 
@@ -741,7 +554,7 @@ void launch_pv(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st,
 }
 
 void launch_combine(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, cudaStream_t stream) {
-  combine_kernel<<<s.n_units * cfg.group, D, 0, stream>>>(s, cfg, st);
+  launch_pdl(combine_kernel, dim3(s.n_units * cfg.group), dim3(D), 0, stream, s, cfg, st);
 }
 
 }  // namespace akv

@@ -347,6 +347,8 @@ template <int G, bool TRUNC>
 __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv_store_t s, akv_cfg_t cfg,
                                                                              akv_step_t st, int cap, float isd,
                                                                              int npg_max) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int HG = QkShape<G>::HG;
   extern __shared__ __align__(16) uint8_t qk_smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -446,7 +448,7 @@ static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
   const long long items = (long long)s.n_units * npg;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + QK_WARPS - 1) / QK_WARPS, 1));
   const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  qk_kernel<G, TRUNC><<<grid, 32 * QK_WARPS, smem, stream>>>(s, cfg, st, cap, isd, npg);
+  launch_pdl(qk_kernel<G, TRUNC>, dim3(grid), dim3(32 * QK_WARPS), smem, stream, s, cfg, st, cap, isd, npg);
 }
 
 void launch_qk(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len, cudaStream_t stream) {

@@ -44,6 +44,8 @@ __device__ __forceinline__ uint32_t v_word_exact(const uint8_t* vp, int tt, int 
 }
 
 __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap) {
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x;
   const int G = cfg.group;
   const int u = h / G;
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
 
 void launch_select(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, cudaStream_t stream) {
   const int cap = s.max_pages * P;
-  select_kernel<<<s.n_units * cfg.group, ST, 0, stream>>>(s, cfg, st, cap);
+  launch_pdl(select_kernel, dim3(s.n_units * cfg.group), dim3(ST), 0, stream, s, cfg, st, cap);
 }
 
 }  // namespace akv
