@@ -30,6 +30,9 @@ struct SelSmem {
   float M, L;
   int ncand, nsel, need_eq, neq;
   unsigned vstar;
+  unsigned wsum[ST / 32];
+  int wfirst[ST / 32];
+  int sel_page[AKV_MAX_KSEL];
   int tmin[4], tunk[4];
 };
 
@@ -43,7 +46,7 @@ __device__ __forceinline__ uint32_t v_word_exact(const uint8_t* vp, int tt, int 
   return (head << 8) | (mid << 4) | low;
 }
 
-__global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap) {
+__global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap) {
   pdl_trigger();
   pdl_wait();
   const int h = blockIdx.x;
@@ -78,6 +81,7 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
   const float M = sm.M, L = sm.L;
   const float pmax = 1.0f / L;  // = expf(0) / L, the argmax token's p
   const float thr = ldexpf(pmax, -cfg.m);
+  const float invL = 1.0f / L;
   const bool est = cfg.force_tier == 0 && cfg.trunc_bits == 0 && cfg.k_sel > 0;  // k_sel = 0: softmax only
   const int k_sel = max(min(cfg.k_sel, AKV_MAX_KSEL), 1);
   const float* sc = st.scores + (size_t)h * cap;
@@ -99,7 +103,11 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
       bool cand = false;
       float p = 0.f;
       if (t < n) {
-        p = expf(sv[b] - M) / L;
+        // exact IEEE division where p can matter; for exp(d) < e^-69 (~1e-30, far below every
+        // threshold, tier boundary and the 1e-3 output tolerance) multiply by 1/L instead, which
+        // keeps the division's denormal slow path out of the common near-one-hot case
+        const float dlt = sv[b] - M;
+        p = dlt > -69.f ? expf(dlt) / L : expf(dlt) * invL;
         pr[t] = p;
         cand = est && p >= thr;
       }
@@ -145,14 +153,32 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
           }
         }
         __syncthreads();
-        if (tid == 0) {
-          int cum = 0, dg = 255;
-          for (; dg > 0; --dg) {
-            if (cum + (int)sm.hist[dg] >= k) break;
-            cum += sm.hist[dg];
+        {
+          // digit of the k-th largest key: scan the histogram from the top bin down
+          // (thread t owns bin 255 - t; block-wide inclusive scan by warp shuffles)
+          const unsigned hv = sm.hist[255 - tid];
+          unsigned incl = hv;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
           }
-          sm.need_eq = k - cum;
-          sm.vstar = prefix | ((unsigned)dg << shift);
+          if (lane == 31) sm.wsum[warp] = incl;
+          __syncthreads();
+          unsigned before = 0;
+          for (int w = 0; w < warp; ++w) before += sm.wsum[w];
+          incl += before;
+          const bool hit = (int)incl >= k || tid == 255;
+          const unsigned hb = __ballot_sync(0xFFFFFFFFu, hit);
+          if (lane == 0) sm.wfirst[warp] = hb ? warp * 32 + __ffs(hb) - 1 : 0x7FFFFFFF;
+          __syncthreads();
+          int first = 0x7FFFFFFF;
+#pragma unroll
+          for (int w = 0; w < ST / 32; ++w) first = min(first, sm.wfirst[w]);
+          if (tid == first) {
+            sm.need_eq = k - (int)(incl - hv);
+            sm.vstar = prefix | ((unsigned)(255 - tid) << shift);
+          }
         }
         __syncthreads();
         k = sm.need_eq;
@@ -215,20 +241,38 @@ __global__ void __launch_bounds__(ST) select_kernel(akv_store_t s, akv_cfg_t cfg
     int rank = 0;
     for (int j = 0; j < cnt; ++j) rank += sm.sel[j] < t;
     sm.sel_sorted[rank] = t;
+    sm.sel_page[rank] = s.page_table[(size_t)u * s.max_pages + t / P];
     atomicOr(bits + (t >> 5), 1u << (t & 31));
   }
   __syncthreads();
-  // rows split over warps (warp w: rows w, w+8, ...), lane = 4 channels; fixed-order reduction
+  // rows split over warps (warp w: rows w, w+8, ...), lane = 4 channels; fixed-order reduction.
+  // Every row's words and p are loaded before the (in-order) accumulation.
   {
+    constexpr int RW = 4;  // rows loaded together (per warp: rows warp + 8r)
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int i = warp; i < cnt; i += ST / 32) {
-      const int t = sm.sel_sorted[i];
-      const uint8_t* vp = page_ptr(s.v_pool, s.page_table, s.max_pages, u, t / P);
-      const float p = pr[t];
+    for (int r0 = 0; warp + r0 * (ST / 32) < cnt; r0 += RW) {
+      float pv[RW];
+      uint32_t wv[RW][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t w = v_word_exact(vp, t % P, lane * 4 + e);
-        acc[e] = fmaf(p, __half2float(__ushort_as_half((unsigned short)w)), acc[e]);
+      for (int r = 0; r < RW; ++r) {
+        const int i = warp + (r0 + r) * (ST / 32);
+        pv[r] = 0.f;
+        wv[r][0] = wv[r][1] = wv[r][2] = wv[r][3] = 0u;
+        if (i < cnt) {
+          const int t = sm.sel_sorted[i];
+          const uint8_t* vp = s.v_pool + (size_t)sm.sel_page[i] * PAGE;
+          pv[r] = pr[t];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) wv[r][e] = v_word_exact(vp, t % P, lane * 4 + e);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        if (warp + (r0 + r) * (ST / 32) < cnt) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            acc[e] = fmaf(pv[r], __half2float(__ushort_as_half((unsigned short)wv[r][e])), acc[e]);
+        }
       }
     }
 #pragma unroll
