@@ -344,21 +344,20 @@ def main():
     except Exception:
         pass
 
-    # ---- end-to-end through the public API with host buffers
+    # ---- end-to-end through the public API with host buffers: attention_decode.DecodeGraph
+    #      (CUDA graph of append + decode); per step H2D of q / k_new / v_new from pinned host
+    #      memory, one graph replay, D2H of o (synchronous)
     e2e = None
     if not args.no_e2e:
-        qh = q.cpu().pin_memory()
-        kh = k_new.cpu().pin_memory()
-        vh = v_new.cpu().pin_memory()
-        oh = torch.empty((B, Hkv * g, d), dtype=torch.float32).pin_memory()
+        dg = AD.DecodeGraph(store, g, rewind_to=n - 1).capture()
+        dg.host_q.copy_(q.cpu())
+        dg.host_k.copy_(k_new.cpu())
+        dg.host_v.copy_(v_new.cpu())
 
         def e2e_step():
-            store.rewind(n - 1)
-            store.append_token(kh, vh)  # strict=False: no host sync inside the step
-            o = AD.decode(qh, store)
+            dg.step()  # graph: H2D q/k/v (pinned) -> append -> decode -> D2H o (pinned), synchronised
             if world > 1:
-                dist.all_gather_into_tensor(gathered, o.view(-1, d))
-            oh.copy_(o)  # D2H (synchronous read of the step's result)
+                dist.all_gather_into_tensor(gathered, dg.o.reshape(-1, d))
 
         for _ in range(args.warmup):
             e2e_step()
@@ -374,10 +373,11 @@ def main():
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        store.check()
+        dg.check()
         e2e = {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(qh.numel() * 2 + kh.numel() * 2 + vh.numel() * 2),
-               "d2h_bytes_per_step": int(oh.numel() * 4)}
+               "h2d_bytes_per_step": dg.h2d_bytes, "d2h_bytes_per_step": dg.d2h_bytes,
+               "api": "attention_decode.DecodeGraph.step (CUDA graph: H2D q/k/v + append + qk + select + pv + "
+                      "combine + D2H o)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -402,3 +402,110 @@ def decode(q, store: KVStore, cfg: AlignConfig = AlignConfig(), *, k_sel: int = 
 
 def check_status(store: KVStore, group: int) -> None:
     _raise_status(store.workspace(group), store)
+
+
+class DecodeGraph:
+    """One serving decode step captured as a CUDA graph: H2D of the step's
+    q / k_new / v_new from pinned host buffers, append the new token's K/V,
+    aligned attention (qk, select, pv, combine), D2H of o into a pinned host
+    buffer.
+
+        g = DecodeGraph(store, group=1).capture()
+        g.host_q.copy_(q); g.host_k.copy_(k_new); g.host_v.copy_(v_new)   # or g.step(q, k_new, v_new)
+        o = g.step()                                                        # replay + synchronise
+
+    Each replay appends one token per unit (the host length mirror advances)
+    and returns o [B, Hq, d] fp32 on the host.  Data-dependent errors stay on
+    device: call `check()` to raise them (non-finite K/V, degenerate q).
+    `rewind_to` (benchmarks only) captures a reset of every unit's length
+    before the append, so every replay attends over the same n tokens.  The
+    grid is sized for the store's capacity (fixed at capture).
+    """
+
+    def __init__(self, store: KVStore, group: int = 1, cfg: AlignConfig = AlignConfig(), *, k_sel: int = 32,
+                 m: int = 5, strategy: str = ELEMENT, force_tier=None, rewind_to: Optional[int] = None):
+        self.store, self.group = store, group
+        self.rewind_to = rewind_to
+        B, H, d, dev = store.batch, store.n_kv_heads, store.n_dims, store.device
+        self.q = torch.zeros((B, H * group, d), dtype=torch.int16, device=dev)
+        self.k = torch.zeros((B, H, d), dtype=torch.int16, device=dev)
+        self.v = torch.zeros((B, H, d), dtype=torch.int16, device=dev)
+        self.host_q = torch.zeros(self.q.shape, dtype=torch.int16).pin_memory()
+        self.host_k = torch.zeros(self.k.shape, dtype=torch.int16).pin_memory()
+        self.host_v = torch.zeros(self.v.shape, dtype=torch.int16).pin_memory()
+        self.host_o = torch.zeros((B, H * group, d), dtype=torch.float32).pin_memory()
+        self.ws = store.workspace(group)
+        self.ws.set_v_tiers(False)
+        self.cfg_c = make_cfg(group, cfg, k_sel, m, strategy, force_tier)
+        self.o = self.ws.o.view(B, H * group, d)
+        self.graph = None
+        self._L = _lib.lib()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 2 * (self.host_q.numel() + self.host_k.numel() + self.host_v.numel())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 4 * self.host_o.numel()
+
+    def _enqueue(self, stream_ptr: int):
+        st = self.store
+        self.q.copy_(self.host_q, non_blocking=True)
+        self.k.copy_(self.host_k, non_blocking=True)
+        self.v.copy_(self.host_v, non_blocking=True)
+        if self.rewind_to is not None:
+            st.lengths_dev.fill_(self.rewind_to)
+        _lib.check(self._L.akv_append(ctypes.byref(st.c_store), self.k.data_ptr(), self.v.data_ptr(), 1,
+                                      st.status_dev.data_ptr(), stream_ptr), "akv_append")
+        self.ws.step.q = self.q.data_ptr()
+        _lib.check(self._L.akv_decode_step(ctypes.byref(st.c_store), ctypes.byref(self.cfg_c),
+                                           ctypes.byref(self.ws.step), st.capacity, stream_ptr), "akv_decode_step")
+        self.host_o.copy_(self.o, non_blocking=True)
+
+    def capture(self):
+        st = self.store
+        n0 = int(st._host_len.max()) if self.rewind_to is None else self.rewind_to
+        if n0 + 1 > st.capacity:
+            raise ValueError("store is full")
+        st.check()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=st.device)
+        s.wait_stream(torch.cuda.current_stream(st.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._enqueue(s.cuda_stream)
+        torch.cuda.current_stream(st.device).wait_stream(s)
+        self.graph = g
+        return self
+
+    def _advance(self):
+        st = self.store
+        if self.rewind_to is not None:
+            st._host_len[:] = self.rewind_to + 1
+        else:
+            st._host_len += 1
+
+    def step(self, q=None, k_new=None, v_new=None) -> torch.Tensor:
+        """Optionally copy q / k_new / v_new into the pinned host buffers, replay, return host o."""
+        if self.graph is None:
+            self.capture()
+        for src, dst in ((q, self.host_q), (k_new, self.host_k), (v_new, self.host_v)):
+            if src is not None:
+                dst.copy_(_as_bits(src, torch.device("cpu")).view(dst.shape))
+        self.graph.replay()
+        self._advance()
+        torch.cuda.current_stream(self.store.device).synchronize()
+        return self.host_o
+
+    def check(self):
+        """Raise the device-side status of the last replay (non-finite K/V, degenerate q)."""
+        st = self.store
+        s = st.status_dev.cpu().numpy()
+        bad = np.nonzero(s)[0]
+        if bad.size:
+            code, isv, c, t = decode_status(int(s[bad[0]]))
+            b, h = divmod(int(bad[0]), st.n_kv_heads)
+            raise ValueError(f"append failed: status code {code} ({'V' if isv else 'K'}) at batch {b}, "
+                             f"kv-head {h}, channel {c}")
+        _raise_status(self.ws, st)

@@ -19,6 +19,7 @@ from oracle.analysis import relative_error_histogram
 from oracle.kv_store import PlaneTensor as OPlane
 from paper_2409_16546_b200 import AlignConfig, DegenerateInputError, KVStore
 from paper_2409_16546_b200 import attention_decode as AD
+from paper_2409_16546_b200.synth import generate_batch
 from tests.gpu_helpers import Case, close
 
 
@@ -261,3 +262,28 @@ def test_determinism_and_ragged_lengths():
         assert close(r.o[0, 2 + j].cpu().numpy(), ref.o)
     # the untouched units are unchanged
     assert torch.equal(r.o[0, :2], a.o[0, :2]) and torch.equal(r.o[1], a.o[1])
+
+
+def test_decode_graph_matches_decode_step():
+    """DecodeGraph (CUDA graph of append + decode) == eager append_token + decode_step."""
+    B, Hkv, g, n = 2, 2, 2, 500
+    K, V, Q = generate_batch(B, Hkv, n, 128, g, 5)
+    d = 128
+    kt = torch.from_numpy(K.view(np.int16)).view(B, Hkv, n, d)
+    vt = torch.from_numpy(V.view(np.int16)).view(B, Hkv, n, d)
+    q = torch.from_numpy(Q.view(np.int16)).view(B, Hkv * g, d)
+    a = KVStore(B, Hkv, d, 512)
+    a.append(kt[:, :, : n - 1], vt[:, :, : n - 1])
+    a.append_token(kt[:, :, n - 1], vt[:, :, n - 1])
+    ref = AD.decode_step(q, a)
+    b = KVStore(B, Hkv, d, 512)
+    b.append(kt[:, :, : n - 1], vt[:, :, : n - 1])
+    dg = AD.DecodeGraph(b, g, rewind_to=n - 1).capture()
+    for _ in range(3):  # replays are idempotent with rewind_to
+        out = dg.step(q, kt[:, :, n - 1], vt[:, :, n - 1])
+    dg.check()
+    assert torch.equal(out, ref.o.cpu())
+    # in-place host buffers (the serving form): fill, replay, read
+    dg.host_q.copy_(q)
+    out2 = dg.step()
+    assert torch.equal(out2, ref.o.cpu())
