@@ -57,93 +57,52 @@ struct PvCtx {
   uint32_t nwu;       // lanes 0..7: union need-mid word of chunk lane; lanes 8..15: need-low word of chunk lane-8
 };
 
-template <int G, int HG, bool TRUNC, bool EXPORT, bool UNIFORM>
-__device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const PvCtx& c, int b, int j0, const akv_cfg_t& cfg,
-                                          const akv_step_t& st, float2 (&acc)[HG][8], int (&adj)[HG][3],
-                                          int (&base)[HG], uint32_t tkm, uint32_t tf) {
+template <int HG>
+struct VGen {  // contributions of the aligned generic path (returned by value: keeps the caller's
+  float2 acc[HG][8];  // accumulators in registers)
+  int adj[HG][3];
+};
+template <int HG>
+struct VRowP {
+  float v[HG][4];
+};
+
+// Aligned rows of a batch in the union fetch plan: per q-head mode (selected -> skip,
+// no need bit -> T8, row strategy -> row tier, element strategy -> per-element rule D4),
+// nibble rows fetched here.  Rare on the hot path, so kept out of line (I-cache).
+template <int G, int HG, bool EXPORT>
+__device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c, int b, int j0, akv_cfg_t cfg,
+                                                   const akv_step_t* stp, VRowP<HG> p, uint32_t um) {
+  const akv_step_t& st = *stp;
   const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
-  constexpr bool aligned = !UNIFORM;
-  const int uni = TRUNC ? 16 : cfg.force_tier;
   const int ch = b >> 1, sh16 = 16 * (b & 1);
   const int nvalid = min(max(c.rows - 16 * b, 0), 16);
-  const uint32_t vmask16 = nvalid >= 16 ? 0xFFFFu : ((1u << nvalid) - 1u);
-  const uint32_t um = __shfl_sync(0xFFFFFFFFu, c.nwu, ch);
   const int capw = c.cap >> 5;
-  // p of this lane's 4 rows per head; the selection (D6) and the page end fold into p = 0
-  float p[HG][4];
+  VGen<HG> out;
 #pragma unroll
   for (int jj = 0; jj < HG; ++jj) {
-    const uint32_t selb = aligned ? ((X.sel[jj] >> sh16) & vmask16) : 0u;
-    base[jj] += nvalid - __popc(selb);  // rows counted at T8 (aligned) / the uniform tier
+    out.adj[jj][0] = out.adj[jj][1] = out.adj[jj][2] = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rr = 4 * i + r4;
-      const float pv = __shfl_sync(0xFFFFFFFFu, X.p[jj], rr);
-      p[jj][i] = ((selb >> rr) & 1u) ? 0.f : pv;
-    }
+    for (int q = 0; q < 8; ++q) out.acc[jj][q] = make_float2(0.f, 0.f);
   }
   uint8_t* vt = nullptr;
   if (EXPORT && st.v_tiers) vt = st.v_tiers + ((size_t)c.u * G * c.cap + (size_t)c.pg * P + 16 * b) * D + cg * 16;
-
-  if (aligned && ((um >> sh16) & vmask16) == 0u) {
-    // fast batch: every row is T8 (or p = 0) for every q-head
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t w[8];
-      t8_words16(X.h[i], w);
-      float2 f[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
-#pragma unroll
-      for (int jj = 0; jj < HG; ++jj)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], p[jj][i], acc[jj][k]);
-      if (EXPORT && vt) {
-        const int rr = 4 * i + r4;
-        if (rr < nvalid) {
-#pragma unroll
-          for (int jj = 0; jj < HG; ++jj) {
-            const bool sel = (X.sel[jj] >> (sh16 + rr)) & 1u;
-            const uint32_t cd = sel ? 0x10101010u : 0x08080808u;
-            *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) = make_uint4(cd, cd, cd, cd);
-          }
-        }
-      }
-    }
-    return;
-  }
-  // generic rows (some row of the batch needs a nibble for some q-head, or a forced tier).
-  // Aligned mode fetches the needed nibble rows here (union fetch plan).
-  uint2 mw[4], lw[4];
-  if (UNIFORM) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      mw[i] = X.m[UNIFORM ? i : 0];
-      lw[i] = X.l[UNIFORM ? i : 0];
-    }
-  } else {
-    const uint32_t ul = __shfl_sync(0xFFFFFFFFu, c.nwu, 8 + ch);
-    const uint64_t pol = evict_first_policy();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = 16 * b + 4 * i + r4;
-      mw[i] = make_uint2(0u, 0u);
-      lw[i] = make_uint2(0u, 0u);
-      if (row < c.rows && ((um >> (row & 31)) & 1u)) mw[i] = ld_stream_u64(c.vb + MID + row * (D / 2) + cg * 8, pol);
-      if (row < c.rows && ((ul >> (row & 31)) & 1u)) lw[i] = ld_stream_u64(c.vb + LOW + row * (D / 2) + cg * 8, pol);
-    }
-  }
-#pragma unroll
+  const uint32_t ul = __shfl_sync(0xFFFFFFFFu, c.nwu, 8 + ch);
+  const uint64_t pol = evict_first_policy();
+#pragma unroll 1
   for (int i = 0; i < 4; ++i) {
     const int rr = 4 * i + r4, row = 16 * b + rr;
     const bool valid = rr < nvalid;
+    const uint4 hv = i == 0 ? X.h[0] : (i == 1 ? X.h[1] : (i == 2 ? X.h[2] : X.h[3]));
+    uint2 mw = make_uint2(0u, 0u), lw = make_uint2(0u, 0u);
+    if (valid && ((um >> (row & 31)) & 1u)) mw = ld_stream_u64(c.vb + MID + row * (D / 2) + cg * 8, pol);
+    if (valid && ((ul >> (row & 31)) & 1u)) lw = ld_stream_u64(c.vb + LOW + row * (D / 2) + cg * 8, pol);
 #pragma unroll
     for (int jj = 0; jj < HG; ++jj) {
       const size_t h = (size_t)c.u * G + j0 + jj;
+      const float pv = i == 0 ? p.v[jj][0] : (i == 1 ? p.v[jj][1] : (i == 2 ? p.v[jj][2] : p.v[jj][3]));
       int mode;  // 0 skip, 1 element, 8/12/16 tier
-      if (!aligned) {
-        mode = uni;
-      } else if ((X.sel[jj] >> (sh16 + rr)) & 1u) {
+      if ((X.sel[jj] >> (sh16 + rr)) & 1u) {
         mode = 0;
       } else {
         const uint32_t nm = st.need_bits[h * 2 * capw + c.pg * 8 + ch];
@@ -160,28 +119,24 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
       uint32_t w[8];
       uint32_t cds[4] = {0u, 0u, 0u, 0u};
       if (mode == 0) {
-        if (EXPORT && vt && valid) {
+        if (EXPORT && vt && valid)
           *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) =
               make_uint4(0x10101010u, 0x10101010u, 0x10101010u, 0x10101010u);
-        }
         continue;
       }
       if (mode == 8) {
-        t8_words16(X.h[i], w);
+        t8_words16(hv, w);
         if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = 0x08080808u;
       } else if (mode != 1) {
         const TierMask tm = tier_mask(mode);
-        assemble8(X.h[i].x, X.h[i].y, bsel(tm.mk, mw[i].x, 0x88888888u), bsel(tm.lk, lw[i].x, tm.lf), w);
-        assemble8(X.h[i].z, X.h[i].w, bsel(tm.mk, mw[i].y, 0x88888888u), bsel(tm.lk, lw[i].y, tm.lf), w + 4);
-        if (aligned) {
-          adj[jj][0] -= 16;
-          adj[jj][mode == 12 ? 1 : 2] += 16;
-        }
+        assemble8(hv.x, hv.y, bsel(tm.mk, mw.x, 0x88888888u), bsel(tm.lk, lw.x, tm.lf), w);
+        assemble8(hv.z, hv.w, bsel(tm.mk, mw.y, 0x88888888u), bsel(tm.lk, lw.y, tm.lf), w + 4);
+        out.adj[jj][0] -= 16;
+        out.adj[jj][mode == 12 ? 1 : 2] += 16;
         if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = (uint32_t)mode * 0x01010101u;
       } else {
-        assemble8(X.h[i].x, X.h[i].y, mw[i].x, lw[i].x, w);
-        assemble8(X.h[i].z, X.h[i].w, mw[i].y, lw[i].y, w + 4);
-        const float pv = p[jj][i];
+        assemble8(hv.x, hv.y, mw.x, lw.x, w);
+        assemble8(hv.z, hv.w, mw.y, lw.y, w + 4);
         const int ep = pv > 0.f ? floor_log2f(pv) : -30000;
         const int4* tp = reinterpret_cast<const int4*>(st.targets + h * D + cg * 16);
         int tg[16];
@@ -193,7 +148,7 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
           tg[4 * q4 + 2] = t.z;
           tg[4 * q4 + 3] = t.w;
         }
-        const uint32_t hb[4] = {X.h[i].x, X.h[i].y, X.h[i].z, X.h[i].w};
+        const uint32_t hb[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int g = tg[e] == AKV_TARGET_UNKNOWN ? -(1 << 20) : 17 + tg[e] - cfg.margin_bits;
@@ -204,22 +159,118 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
           uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
           w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
           w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
-          adj[jj][0] -= km ? 1 : 0;
-          adj[jj][1] += (km && !kl) ? 1 : 0;
-          adj[jj][2] += kl ? 1 : 0;
+          out.adj[jj][0] -= km ? 1 : 0;
+          out.adj[jj][1] += (km && !kl) ? 1 : 0;
+          out.adj[jj][2] += kl ? 1 : 0;
           if (EXPORT) cds[e >> 2] |= (kl ? 16u : (km ? 12u : 8u)) << (8 * (e & 3));
         }
       }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) out.acc[jj][k] = ffma2_scalar(half2_bits_to_float2(w[k]), pv, out.acc[jj][k]);
+      if (EXPORT && vt)
+        *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) =
+            make_uint4(cds[0], cds[1], cds[2], cds[3]);
+    }
+  }
+  return out;
+}
+
+template <int G, int HG, bool TRUNC, bool EXPORT, bool UNIFORM>
+__device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const PvCtx& c, int b, int j0, const akv_cfg_t& cfg,
+                                          const akv_step_t& st, float2 (&acc)[HG][8], int (&adj)[HG][3],
+                                          int (&base)[HG], uint32_t tkm, uint32_t tf) {
+  const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
+  constexpr bool aligned = !UNIFORM;
+  const int uni = TRUNC ? 16 : cfg.force_tier;
+  const int ch = b >> 1, sh16 = 16 * (b & 1);
+  const int nvalid = min(max(c.rows - 16 * b, 0), 16);
+  const uint32_t vmask16 = nvalid >= 16 ? 0xFFFFu : ((1u << nvalid) - 1u);
+  const uint32_t um = __shfl_sync(0xFFFFFFFFu, c.nwu, ch);
+  // p of this lane's 4 rows per head; the selection (D6) and the page end fold into p = 0
+  VRowP<HG> p;
+#pragma unroll
+  for (int jj = 0; jj < HG; ++jj) {
+    const uint32_t selb = aligned ? ((X.sel[jj] >> sh16) & vmask16) : 0u;
+    base[jj] += nvalid - __popc(selb);  // rows counted at T8 (aligned) / the uniform tier
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = 4 * i + r4;
+      const float pv = __shfl_sync(0xFFFFFFFFu, X.p[jj], rr);
+      p.v[jj][i] = ((selb >> rr) & 1u) || rr >= nvalid ? 0.f : pv;
+    }
+  }
+  uint8_t* vt = nullptr;
+  if (EXPORT && st.v_tiers) vt = st.v_tiers + ((size_t)c.u * G * c.cap + (size_t)c.pg * P + 16 * b) * D + cg * 16;
+
+  if (UNIFORM) {
+    // forced / baseline tier: one mask for every valid row
+    const TierMask tm = tier_mask(uni);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w[8];
+      const uint2 mw = X.m[UNIFORM ? i : 0], lw = X.l[UNIFORM ? i : 0];
+      assemble8(X.h[i].x, X.h[i].y, bsel(tm.mk, mw.x, 0x88888888u), bsel(tm.lk, lw.x, tm.lf), w);
+      assemble8(X.h[i].z, X.h[i].w, bsel(tm.mk, mw.y, 0x88888888u), bsel(tm.lk, lw.y, tm.lf), w + 4);
       if (TRUNC) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = (w[k] & tkm) | tf;
       }
-      const float pv = p[jj][i];
+      float2 f[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(half2_bits_to_float2(w[k]), pv, acc[jj][k]);
-      if (EXPORT && vt)
-        *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) =
-            make_uint4(cds[0], cds[1], cds[2], cds[3]);
+      for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], p.v[jj][i], acc[jj][k]);
+      if (EXPORT && vt && 4 * i + r4 < nvalid) {
+        const uint32_t cd = (uint32_t)uni * 0x01010101u;
+#pragma unroll
+        for (int jj = 0; jj < HG; ++jj)
+          *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)(4 * i + r4) * D) =
+              make_uint4(cd, cd, cd, cd);
+      }
+    }
+    return;
+  }
+  if (((um >> sh16) & vmask16) == 0u) {
+    // fast batch: every row is T8 (or p = 0) for every q-head
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w[8];
+      t8_words16(X.h[i], w);
+      float2 f[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], p.v[jj][i], acc[jj][k]);
+      if (EXPORT && vt) {
+        const int rr = 4 * i + r4;
+        if (rr < nvalid) {
+#pragma unroll
+          for (int jj = 0; jj < HG; ++jj) {
+            const bool sel = (X.sel[jj] >> (sh16 + rr)) & 1u;
+            const uint32_t cd = sel ? 0x10101010u : 0x08080808u;
+            *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) = make_uint4(cd, cd, cd, cd);
+          }
+        }
+      }
+    }
+    return;
+  }
+  if constexpr (!UNIFORM) {
+    const VGen<HG> gen = v_generic_aligned<G, HG, EXPORT>(X, c, b, j0, cfg, &st, p, um);
+#pragma unroll
+    for (int jj = 0; jj < HG; ++jj) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        acc[jj][k].x += gen.acc[jj][k].x;
+        acc[jj][k].y += gen.acc[jj][k].y;
+      }
+      adj[jj][0] += gen.adj[jj][0];
+      adj[jj][1] += gen.adj[jj][1];
+      adj[jj][2] += gen.adj[jj][2];
     }
   }
 }
@@ -235,7 +286,7 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
 // ---------------------------------------------------------------------------
 template <int G, bool UNIFORM>
 struct Pv3Shape {
-  static constexpr int HG = G < 4 ? G : 4;
+  static constexpr int HG = G < 2 ? G : 2;  // q-heads per pass (registers / I-cache); passes re-read the page from L2
   static constexpr int NPASS = G / HG;
   static constexpr int ROWS = UNIFORM ? 32 : 64;                 // rows per stage
   static constexpr int HEAD = ROWS * D;                          // head bytes per stage

@@ -37,7 +37,7 @@ constexpr int QK_WARPS = 4;  // warps per CTA
 template <int G>
 struct QkShape {
   // resident CTAs per SM (register budget: 64K / (128 threads * MINB))
-  static constexpr int HG = G < 4 ? G : 4;          // q-heads per pass over a page (accumulator budget)
+  static constexpr int HG = G < 2 ? G : 2;          // q-heads per pass over a page (registers / I-cache; later passes hit L2)
   static constexpr int MINB = G == 1 ? 3 : 2;
 };
 
