@@ -14,8 +14,12 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   pdl_wait();
   const int u = blockIdx.x;
   const int c = threadIdx.x;
+  // independent loads first (k, v, length), then the page id: two dependent round trips in all
   const uint32_t kw = k[(size_t)u * D + c];
   const uint32_t vw = v[(size_t)u * D + c];
+  const int t = s.lengths[u];
+  const bool room = t < s.max_pages * P;
+  const size_t pid = room ? (size_t)s.page_table[(size_t)u * s.max_pages + t / P] : 0;
   __shared__ int s_bad;
   __shared__ uint32_t s_rowmax;
   if (c == 0) {
@@ -26,8 +30,8 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   // first offending element: K before V, lowest channel (matches the oracle's argwhere order)
   if (!finite16(kw)) atomicMin(&s_bad, c);
   if (!finite16(vw)) atomicMin(&s_bad, 0x100 | c);
+  atomicMax(&s_rowmax, vw & 0x7FFFu);
   __syncthreads();
-  const int t = s.lengths[u];
   if (s_bad != 0x7FFFFFFF) {
     if (c == 0) {
       const int bad = s_bad;
@@ -35,26 +39,30 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
     }
     return;
   }
-  if (t >= s.max_pages * P) {
+  if (!room) {
     if (c == 0) status[u] = status_word(AKV_STATUS_CAPACITY, t);
     return;
   }
-  if (c == 0) status[u] = 0;
   const int tt = t % P;
-  uint8_t* kp = s.k_pool + (size_t)s.page_table[(size_t)u * s.max_pages + t / P] * PAGE;
-  uint8_t* vp = s.v_pool + (size_t)s.page_table[(size_t)u * s.max_pages + t / P] * PAGE;
+  uint8_t* kp = s.k_pool + pid * PAGE;
+  uint8_t* vp = s.v_pool + pid * PAGE;
 
-  // K: channel-major planes; one byte of each nibble plane is shared with
-  // token tt^4 of the same 8-group, written at another step (single writer).
+  // K: channel-major planes.  A nibble word holds 4 token positions of this
+  // channel only, so the update is two fire-and-forget reductions (clear, set)
+  // instead of a read-modify-write round trip (same-address atomics of one
+  // thread are ordered).
   kp[c * P + tt] = (uint8_t)(kw >> 8);
   {
-    const int byte = c * (P / 2) + (tt >> 3) * 4 + (tt & 3);
+    const int word = (c * (P / 2) + (tt >> 3) * 4) >> 2;
     const bool first = (tt & 7) < 4;
-    uint8_t* mb = kp + MID + byte;
-    uint8_t* lb = kp + LOW + byte;
-    const uint32_t mn = (kw >> 4) & 0xF, ln = kw & 0xF;
-    *mb = first ? (uint8_t)((*mb & 0x0F) | (mn << 4)) : (uint8_t)((*mb & 0xF0) | mn);
-    *lb = first ? (uint8_t)((*lb & 0xF0) | ln) : (uint8_t)((*lb & 0x0F) | (ln << 4));
+    const int sh = 8 * (tt & 3);
+    const int shm = sh + (first ? 4 : 0), shl = sh + (first ? 0 : 4);
+    unsigned int* mw = reinterpret_cast<unsigned int*>(kp + MID) + word;
+    unsigned int* lw = reinterpret_cast<unsigned int*>(kp + LOW) + word;
+    atomicAnd(mw, ~(0xFu << shm));
+    atomicOr(mw, ((kw >> 4) & 0xFu) << shm);
+    atomicAnd(lw, ~(0xFu << shl));
+    atomicOr(lw, (kw & 0xFu) << shl);
   }
   // V: token-major planes; channel c pairs with c+4 inside its 8-group.
   vp[tt * D + c] = (uint8_t)(vw >> 8);
@@ -68,12 +76,10 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
       vp[LOW + byte] = (uint8_t)(ln | (ln4 << 4));
     }
   }
-  // sidecars
-  uint32_t* cm = s.colmax + (size_t)u * D + c;
-  *cm = max(*cm, kw & 0x7FFFu);
-  atomicMax(&s_rowmax, vw & 0x7FFFu);
-  __syncthreads();
+  // sidecars: ColMax by reduction, RowMax from the block max
+  atomicMax(s.colmax + (size_t)u * D + c, kw & 0x7FFFu);
   if (c == 0) {
+    status[u] = 0;
     s.rowmax[(size_t)u * s.max_pages * P + t] = (uint16_t)s_rowmax;
     s.lengths[u] = t + 1;
   }
