@@ -286,7 +286,7 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
 // ---------------------------------------------------------------------------
 template <int G, bool UNIFORM>
 struct Pv3Shape {
-  static constexpr int HG = G < 2 ? G : 2;  // q-heads per pass (registers / I-cache); passes re-read the page from L2
+  static constexpr int HG = G < 4 ? G : 4;  // q-heads per pass (accumulator budget); passes re-read the page from L2
   static constexpr int NPASS = G / HG;
   static constexpr int ROWS = UNIFORM ? 32 : 64;                 // rows per stage
   static constexpr int HEAD = ROWS * D;                          // head bytes per stage
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
     }
     const float* sp = reinterpret_cast<const float*>(md + S::M_P);
     const uint32_t* ss = reinterpret_cast<const uint32_t*>(md + S::M_SEL);
-#pragma unroll
+#pragma unroll(G == 1 ? S::ROWS / 16 : 1)
     for (int bb = 0; bb < S::ROWS / 16; ++bb) {
       const int b = cc.sub * (S::ROWS / 16) + bb;  // 16-row batch index inside the page
       if (16 * b >= c.rows) break;

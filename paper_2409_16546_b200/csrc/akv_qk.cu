@@ -37,7 +37,7 @@ constexpr int QK_WARPS = 4;  // warps per CTA
 template <int G>
 struct QkShape {
   // resident CTAs per SM (register budget: 64K / (128 threads * MINB))
-  static constexpr int HG = G < 2 ? G : 2;          // q-heads per pass over a page (registers / I-cache; later passes hit L2)
+  static constexpr int HG = G < 4 ? G : 4;          // q-heads per pass over a page (accumulator budget)
   static constexpr int MINB = G == 1 ? 3 : 2;
 };
 
@@ -111,6 +111,10 @@ __device__ __forceinline__ void k_load(KBatch& X, const QkWarp<G>& ws, int b, bo
       X.m[i] = ld_stream_u64(mrow, pol);
       X.l[i] = make_uint2(0x88888888u, 0x88888888u);
       if ((lowm >> i) & 1u) X.l[i] = ld_stream_u64(mrow + (LOW - MID), pol);
+    } else if (G > 1) {
+      // T8 words through the full rebuild: mid nibble 8, low nibble 0 = the 0x80 midpoint fill
+      X.m[i] = make_uint2(0x88888888u, 0x88888888u);
+      X.l[i] = make_uint2(0u, 0u);
     }
   }
 }
@@ -396,8 +400,8 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
       KBatch X[3];
       auto load = [&](int b, KBatch& B) { k_load<G>(B, ws, b, b >= nb8, base, l16, half, pol); };
       auto comp = [&](int b, const KBatch& B) {
-        if (b < nb8) k_compute<HG, false, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);
-        else k_compute<HG, true, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);
+        if (G > 1 || b >= nb8) k_compute<HG, true, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);
+        else k_compute<HG, false, TRUNC, G>(B, ws, b, half, j0, acc, tkm, tf);  // G = 1: lighter T8 rebuild
       };
       if (nb > 0) load(0, X[0]);
       if (nb > 1) load(1, X[1]);
