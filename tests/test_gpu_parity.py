@@ -287,3 +287,23 @@ def test_decode_graph_matches_decode_step():
     dg.host_q.copy_(q)
     out2 = dg.step()
     assert torch.equal(out2, ref.o.cpu())
+
+
+def test_many_units_items_span_warps_and_units():
+    """B=16 x 32 kv-heads x 4 pages = 2048 (unit, page) items, more than resident warps:
+    warps cross unit boundaries (Rule-1 re-evaluation, page-table rows, TMA ring cursors)."""
+    c = Case(B=16, Hkv=32, g=1, n=1024, seed=77)
+    r = c.gpu()
+    kt = r.k_tiers.cpu().numpy()
+    o = r.o.cpu().numpy()
+    for u, b, hq, j in c.units():
+        if u % 8:  # oracle on every 8th unit keeps the CPU side to seconds
+            continue
+        ref = c.oracle(u, j)
+        assert np.array_equal(kt[b, hq], ref.k_tiers), u
+        assert close(o[b, hq], ref.o), u
+
+
+def test_gqa_many_pages():
+    """GQA g=4 over 6 pages per unit (two q-head passes are not needed: g <= 4)."""
+    _compare_case(Case(B=2, Hkv=4, g=4, n=1500, seed=91))
