@@ -434,9 +434,232 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
   }
 }
 
+// ---------------------------------------------------------------------------
+// qk v3: per-warp cp.async ring.  Each warp copies its 8-channel batches
+// (head rows, and the T12/T16 channels' mid / low rows) into a private ring of
+// NB shared-memory slots with 16-byte cp.async (one commit group per batch),
+// NB-1 batches ahead of the math, continuing across the pages of a unit; the
+// in-flight data lives in shared memory instead of registers, so more of it
+// fits.  The math reads the slot (LDS.128 / LDS.64) and reuses k_compute.
+// ---------------------------------------------------------------------------
+constexpr int Q3_SLOT = 4096;  // 8 channels: head [8][256 B] | mid [8][128 B] | low [8][128 B]
+
+template <int G>
+struct Qk3Shape {
+  static constexpr int HG = G < 4 ? G : 4;
+  static constexpr int NB = 4;  // ring slots per warp
+  static constexpr int WARPS = 4;
+  static constexpr int LIST = (sizeof(QkWarp<G>) + 127) & ~127;
+  static constexpr int PER_WARP = LIST + NB * Q3_SLOT;
+  static constexpr int SMEM = WARPS * PER_WARP;
+  static constexpr int MINB = G == 1 ? 3 : 2;
+};
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ void q3_issue(uint8_t* slot, const QkWarp<G>& ws, int b, bool full, const uint8_t* base) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
+  const uint4 o = *reinterpret_cast<const uint4*>(&ws.off[8 * b + 4 * half]);
+  const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) cp_async16(slot + (2 * i + half) * 256 + l16 * 16, base + ov[i] + l16 * 16);
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int idx = lane * 2 + k, pib = idx >> 3, chunk = idx & 7;
+      const int sl = 8 * b + 4 * (pib & 1) + (pib >> 1);
+      const uint32_t off = ws.off[sl] >> 1;
+      cp_async16(slot + 2048 + pib * 128 + chunk * 16, base + MID + off + chunk * 16);
+      if ((ws.low[sl >> 5] >> (sl & 31)) & 1u) cp_async16(slot + 3072 + pib * 128 + chunk * 16, base + LOW + off + chunk * 16);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int HG, bool FULL, bool TRUNC, int G>
+__device__ __forceinline__ void q3_compute(const uint8_t* slot, const QkWarp<G>& ws, int b, int j0,
+                                           float (&acc)[HG][16], uint32_t tkm, uint32_t tf) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
+  KBatch X;
+  const uint32_t lowm = FULL ? (ws.low[(8 * b) >> 5] >> ((8 * b + 4 * half) & 31)) & 0xFu : 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int pib = 2 * i + half;
+    X.h[i] = *reinterpret_cast<const uint4*>(slot + pib * 256 + l16 * 16);
+    if (FULL) {
+      X.m[i] = *reinterpret_cast<const uint2*>(slot + 2048 + pib * 128 + l16 * 8);
+      X.l[i] = ((lowm >> i) & 1u) ? *reinterpret_cast<const uint2*>(slot + 3072 + pib * 128 + l16 * 8)
+                                  : make_uint2(0x88888888u, 0x88888888u);
+    } else if (G > 1) {
+      X.m[i] = make_uint2(0x88888888u, 0x88888888u);
+      X.l[i] = make_uint2(0u, 0u);
+    }
+  }
+  k_compute<HG, (FULL || G > 1), TRUNC, G>(X, ws, b, half, j0, acc, tkm, tf);
+}
+
+template <int G, bool TRUNC>
+__global__ void __launch_bounds__(32 * Qk3Shape<G>::WARPS, Qk3Shape<G>::MINB)
+    qk3_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, float isd, int npg_max) {
+  using S = Qk3Shape<G>;
+  constexpr int HG = S::HG, NB = S::NB, NPASS = G / HG;
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(128) uint8_t qk3_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, l16 = lane & 15;
+  QkWarp<G>& ws = *reinterpret_cast<QkWarp<G>*>(qk3_smem + warp * S::PER_WARP);
+  uint8_t* ring = qk3_smem + warp * S::PER_WARP + S::LIST;
+  if (lane == 0) ws.unit = -1;
+  __syncwarp();
+  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
+  if (TRUNC) {
+    const int kb = cfg.trunc_bits - 6;
+    const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
+    const uint32_t fill = kb < 10 ? (1u << (9 - kb)) : 0u;
+    tkm = km | (km << 16);
+    tf = fill | (fill << 16);
+  }
+  // balanced contiguous range of (unit, page, head-pass) items
+  const long long total = (long long)s.n_units * npg_max * NPASS;
+  const long long nw = (long long)gridDim.x * S::WARPS, gw = (long long)blockIdx.x * S::WARPS + warp;
+  const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
+  const int cap_chunks = s.max_pages * (P / 32);
+
+  // load cursor (li, lb) and compute cursor (ci, cb) over (item, batch); both walk the same items
+  UnitPages lup, cup;
+  lup.u = cup.u = -1;
+  lup.n = cup.n = 0;
+  long long li = i0, ci = i0;
+  int lb = 0, cb = 0;
+  const uint8_t* lbase = nullptr;
+  bool lblocked = false;  // the load cursor reached a unit whose Rule-1 lists are not built yet
+  int issued = 0, computed = 0;
+  float acc[HG][16];
+#pragma unroll
+  for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[jj][e] = 0.f;
+
+  // next valid item at or after i (page inside its unit's length)
+  auto seek = [&](long long i, UnitPages& up) -> long long {
+    for (; i < i1; ++i) {
+      const long long pi = i / NPASS;
+      const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
+      if (u != up.u) unit_pages_fetch(up, s, u);
+      if (pg * P < up.n) return i;
+    }
+    return i1;
+  };
+  li = seek(li, lup);
+  ci = li;
+  cup = lup;
+  if (li < i1) {
+    const long long pi = li / NPASS;
+    k_prologue<G, TRUNC>(ws, s, cfg, st, (int)(pi / npg_max), lup.n, pi % npg_max == 0);
+    lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+  }
+  while (ci < i1) {
+    // issue up to NB-1 batches ahead (stop at a unit whose lists are not built)
+    while (li < i1 && !lblocked && issued - computed < NB - 1) {
+      const int nb8 = ws.n8p >> 3;
+      q3_issue<G>(ring + (issued % NB) * Q3_SLOT, ws, lb, lb >= nb8, lbase);
+      ++issued;
+      if (++lb == (ws.nlist >> 3)) {
+        lb = 0;
+        const long long pu = li / NPASS / npg_max;
+        li = seek(li + 1, lup);
+        if (li < i1) {
+          const long long pi = li / NPASS;
+          if (pi / npg_max != pu) lblocked = true;  // new unit: wait for the math to drain
+          else lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+        }
+      }
+    }
+    if (issued == computed) {
+      // drained at a unit boundary: build the next unit's lists, resume loading
+      const long long pi = li / NPASS;
+      k_prologue<G, TRUNC>(ws, s, cfg, st, (int)(pi / npg_max), lup.n, pi % npg_max == 0);
+      lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+      lblocked = false;
+      continue;
+    }
+    const int inflight = issued - computed;  // 1 .. NB-1
+    if (inflight >= 3) cp_async_wait<2>();
+    else if (inflight == 2) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncwarp();
+    const int nb8 = ws.n8p >> 3;
+    const long long pi = ci / NPASS;
+    const int j0 = (int)(ci % NPASS) * HG;
+    const uint8_t* slot = ring + (computed % NB) * Q3_SLOT;
+    if (G > 1 || cb >= nb8) q3_compute<HG, true, TRUNC, G>(slot, ws, cb, j0, acc, tkm, tf);
+    else q3_compute<HG, false, TRUNC, G>(slot, ws, cb, j0, acc, tkm, tf);
+    ++computed;
+    __syncwarp();  // every lane is done with the slot before it is refilled
+    if (++cb == (ws.nlist >> 3)) {
+      // page done: fold the half-warps, scale, store, chunk stats
+      const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
+      if (u != cup.u) unit_pages_fetch(cup, s, u);
+      const int n = cup.n;
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        float mine[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float lo = acc[jj][e] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e], 16);
+          const float hi = acc[jj][e + 8] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e + 8], 16);
+          mine[e] = half ? hi : lo;
+        }
+        const size_t hh = (size_t)u * G + j0 + jj;
+        qk_finish(mine, pg * P + 16 * l16 + 8 * half, n, st.scores + hh * cap, st.page_stats + hh * cap_chunks * 2,
+                  isd);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[jj][e] = 0.f;
+      }
+      cb = 0;
+      ci = seek(ci + 1, cup);
+    }
+  }
+}
+
+// The cp.async-ring variant wins for GQA groups (G >= 4: the register pipeline
+// cannot hold enough batches next to 4 heads' accumulators); for G <= 2 the
+// register pipeline is faster (measured, profiles/r01_history.md).
+
+template <int G, bool TRUNC>
+static void launch_qk3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
+                         cudaStream_t stream) {
+  using S = Qk3Shape<G>;
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(qk3_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk3_kernel<G, TRUNC>, 32 * S::WARPS, S::SMEM);
+    resident = sms * std::max(per, 1);
+  }
+  const int cap = s.max_pages * P;
+  const int npg = (max_len + P - 1) / P;
+  const long long items = (long long)s.n_units * npg * (G / S::HG);
+  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
+  launch_pdl(qk3_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
+}
+
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
+  if (G >= 4) {
+    launch_qk3_t<G, TRUNC>(s, cfg, st, max_len, stream);
+    return;
+  }
   static int resident = 0;
   const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
   if (!resident) {
