@@ -349,7 +349,7 @@ def main():
     #      memory, one graph replay, D2H of o (synchronous)
     e2e = None
     if not args.no_e2e:
-        dg = AD.DecodeGraph(store, g, rewind_to=n - 1).capture()
+        dg = AD.DecodeGraph(store, g, rewind_to=n - 1, zero_copy_out=world == 1).capture()
         dg.host_q.copy_(q.cpu())
         dg.host_k.copy_(k_new.cpu())
         dg.host_v.copy_(v_new.cpu())
@@ -376,8 +376,8 @@ def main():
         dg.check()
         e2e = {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": dg.h2d_bytes, "d2h_bytes_per_step": dg.d2h_bytes,
-               "api": "attention_decode.DecodeGraph.step (CUDA graph: H2D q/k/v + append + qk + select + pv + "
-                      "combine + D2H o)"}
+               "api": "attention_decode.DecodeGraph.step (CUDA graph: one H2D of q|k|v + append + qk + select + pv "
+                      "+ combine; o stored by the combine kernel into pinned host memory (zero-copy D2H) at N=1)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

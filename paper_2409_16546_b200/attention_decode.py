@@ -423,27 +423,41 @@ class DecodeGraph:
     """
 
     def __init__(self, store: KVStore, group: int = 1, cfg: AlignConfig = AlignConfig(), *, k_sel: int = 32,
-                 m: int = 5, strategy: str = ELEMENT, force_tier=None, rewind_to: Optional[int] = None):
+                 m: int = 5, strategy: str = ELEMENT, force_tier=None, rewind_to: Optional[int] = None,
+                 zero_copy_out: bool = True):
         self.store, self.group = store, group
         self.rewind_to = rewind_to
         B, H, d, dev = store.batch, store.n_kv_heads, store.n_dims, store.device
-        self.q = torch.zeros((B, H * group, d), dtype=torch.int16, device=dev)
-        self.k = torch.zeros((B, H, d), dtype=torch.int16, device=dev)
-        self.v = torch.zeros((B, H, d), dtype=torch.int16, device=dev)
-        self.host_q = torch.zeros(self.q.shape, dtype=torch.int16).pin_memory()
-        self.host_k = torch.zeros(self.k.shape, dtype=torch.int16).pin_memory()
-        self.host_v = torch.zeros(self.v.shape, dtype=torch.int16).pin_memory()
+        nq, nk = B * H * group * d, B * H * d
+        # one packed input transfer: q | k_new | v_new
+        self.host_in = torch.zeros(nq + 2 * nk, dtype=torch.int16).pin_memory()
+        self.dev_in = torch.zeros(nq + 2 * nk, dtype=torch.int16, device=dev)
+        self.host_q = self.host_in[:nq].view(B, H * group, d)
+        self.host_k = self.host_in[nq:nq + nk].view(B, H, d)
+        self.host_v = self.host_in[nq + nk:].view(B, H, d)
+        self.q = self.dev_in[:nq].view(B, H * group, d)
+        self.k = self.dev_in[nq:nq + nk].view(B, H, d)
+        self.v = self.dev_in[nq + nk:].view(B, H, d)
         self.host_o = torch.zeros((B, H * group, d), dtype=torch.float32).pin_memory()
         self.ws = store.workspace(group)
         self.ws.set_v_tiers(False)
         self.cfg_c = make_cfg(group, cfg, k_sel, m, strategy, force_tier)
         self.o = self.ws.o.view(B, H * group, d)
+        # zero-copy output: the combine kernel stores o straight into the pinned host buffer
+        # (UVA-mapped), so the step has no separate D2H copy
+        self.zero_copy_out = zero_copy_out
+        self.step_c = _lib.AkvStep()
+        ctypes.pointer(self.step_c)[0] = self.ws.step
+        self.step_c.q = self.q.data_ptr()
+        self.step_c.v_tiers = None
+        if zero_copy_out:
+            self.step_c.o = self.host_o.data_ptr()
         self.graph = None
         self._L = _lib.lib()
 
     @property
     def h2d_bytes(self) -> int:
-        return 2 * (self.host_q.numel() + self.host_k.numel() + self.host_v.numel())
+        return 2 * self.host_in.numel()
 
     @property
     def d2h_bytes(self) -> int:
@@ -451,17 +465,15 @@ class DecodeGraph:
 
     def _enqueue(self, stream_ptr: int):
         st = self.store
-        self.q.copy_(self.host_q, non_blocking=True)
-        self.k.copy_(self.host_k, non_blocking=True)
-        self.v.copy_(self.host_v, non_blocking=True)
+        self.dev_in.copy_(self.host_in, non_blocking=True)
         if self.rewind_to is not None:
             st.lengths_dev.fill_(self.rewind_to)
         _lib.check(self._L.akv_append(ctypes.byref(st.c_store), self.k.data_ptr(), self.v.data_ptr(), 1,
                                       st.status_dev.data_ptr(), stream_ptr), "akv_append")
-        self.ws.step.q = self.q.data_ptr()
         _lib.check(self._L.akv_decode_step(ctypes.byref(st.c_store), ctypes.byref(self.cfg_c),
-                                           ctypes.byref(self.ws.step), st.capacity, stream_ptr), "akv_decode_step")
-        self.host_o.copy_(self.o, non_blocking=True)
+                                           ctypes.byref(self.step_c), st.capacity, stream_ptr), "akv_decode_step")
+        if not self.zero_copy_out:
+            self.host_o.copy_(self.o, non_blocking=True)
 
     def capture(self):
         st = self.store
