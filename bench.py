@@ -376,8 +376,9 @@ def main():
         dg.check()
         e2e = {"value": world * B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": dg.h2d_bytes, "d2h_bytes_per_step": dg.d2h_bytes,
-               "api": "attention_decode.DecodeGraph.step (CUDA graph: one H2D of q|k|v + append + qk + select + pv "
-                      "+ combine; o stored by the combine kernel into pinned host memory (zero-copy D2H) at N=1)"}
+               "api": "attention_decode.DecodeGraph.step (CUDA graph: append + qk + select + pv + combine; the "
+                      "kernels read q / k_new / v_new from pinned host memory and combine stores o into pinned host "
+                      "memory at N=1 (zero-copy PCIe transfers inside the step))"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

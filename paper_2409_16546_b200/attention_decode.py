@@ -424,7 +424,7 @@ class DecodeGraph:
 
     def __init__(self, store: KVStore, group: int = 1, cfg: AlignConfig = AlignConfig(), *, k_sel: int = 32,
                  m: int = 5, strategy: str = ELEMENT, force_tier=None, rewind_to: Optional[int] = None,
-                 zero_copy_out: bool = True):
+                 zero_copy_out: bool = True, zero_copy_in: bool = True):
         self.store, self.group = store, group
         self.rewind_to = rewind_to
         B, H, d, dev = store.batch, store.n_kv_heads, store.n_dims, store.device
@@ -443,12 +443,14 @@ class DecodeGraph:
         self.ws.set_v_tiers(False)
         self.cfg_c = make_cfg(group, cfg, k_sel, m, strategy, force_tier)
         self.o = self.ws.o.view(B, H * group, d)
-        # zero-copy output: the combine kernel stores o straight into the pinned host buffer
-        # (UVA-mapped), so the step has no separate D2H copy
+        # zero-copy I/O (UVA-mapped pinned buffers): append and qk read k_new / v_new / q straight
+        # from host memory and the combine kernel stores o straight into it, so the step has no
+        # separate copy nodes (zero_copy_in / zero_copy_out = False: one packed H2D, one D2H)
         self.zero_copy_out = zero_copy_out
         self.step_c = _lib.AkvStep()
         ctypes.pointer(self.step_c)[0] = self.ws.step
-        self.step_c.q = self.q.data_ptr()
+        self.zero_copy_in = zero_copy_in
+        self.step_c.q = (self.host_q if zero_copy_in else self.q).data_ptr()
         self.step_c.v_tiers = None
         if zero_copy_out:
             self.step_c.o = self.host_o.data_ptr()
@@ -465,10 +467,12 @@ class DecodeGraph:
 
     def _enqueue(self, stream_ptr: int):
         st = self.store
-        self.dev_in.copy_(self.host_in, non_blocking=True)
+        if not self.zero_copy_in:
+            self.dev_in.copy_(self.host_in, non_blocking=True)
         if self.rewind_to is not None:
             st.lengths_dev.fill_(self.rewind_to)
-        _lib.check(self._L.akv_append(ctypes.byref(st.c_store), self.k.data_ptr(), self.v.data_ptr(), 1,
+        kk, vv = (self.host_k, self.host_v) if self.zero_copy_in else (self.k, self.v)
+        _lib.check(self._L.akv_append(ctypes.byref(st.c_store), kk.data_ptr(), vv.data_ptr(), 1,
                                       st.status_dev.data_ptr(), stream_ptr), "akv_append")
         _lib.check(self._L.akv_decode_step(ctypes.byref(st.c_store), ctypes.byref(self.cfg_c),
                                            ctypes.byref(self.step_c), st.capacity, stream_ptr), "akv_decode_step")

@@ -307,3 +307,21 @@ def test_many_units_items_span_warps_and_units():
 def test_gqa_many_pages():
     """GQA g=4 over 6 pages per unit (two q-head passes are not needed: g <= 4)."""
     _compare_case(Case(B=2, Hkv=4, g=4, n=1500, seed=91))
+
+
+@pytest.mark.parametrize("zin,zout", [(False, False), (True, False), (False, True)])
+def test_decode_graph_copy_modes(zin, zout):
+    B, Hkv, g, n = 2, 2, 1, 300
+    K, V, Q = generate_batch(B, Hkv, n, 128, g, 6)
+    d = 128
+    kt = torch.from_numpy(K.view(np.int16)).view(B, Hkv, n, d)
+    vt = torch.from_numpy(V.view(np.int16)).view(B, Hkv, n, d)
+    q = torch.from_numpy(Q.view(np.int16)).view(B, Hkv * g, d)
+    a = KVStore(B, Hkv, d, 512)
+    a.append(kt, vt)
+    ref = AD.decode_step(q, a)
+    b = KVStore(B, Hkv, d, 512)
+    b.append(kt[:, :, : n - 1], vt[:, :, : n - 1])
+    dg = AD.DecodeGraph(b, g, rewind_to=n - 1, zero_copy_in=zin, zero_copy_out=zout).capture()
+    out = dg.step(q, kt[:, :, n - 1], vt[:, :, n - 1])
+    assert torch.equal(out, ref.o.cpu())
