@@ -480,6 +480,43 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
     }
     const float* sp = reinterpret_cast<const float*>(md + S::M_P);
     const uint32_t* ss = reinterpret_cast<const uint32_t*>(md + S::M_SEL);
+    if (!UNIFORM && cc.sub == 0 && !EXPORT) {
+      // page start: fold the selection (D6) and the page end into the staged p (p = 0 there),
+      // so the stage fast path below reads p without masks
+      float* spw = reinterpret_cast<float*>(metab + (cc.npage & 1) * S::META + S::M_P);
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+        for (int r = lane; r < P; r += 32)
+          if (r >= c.rows || ((ss[jj * 8 + (r >> 5)] >> (r & 31)) & 1u)) spw[jj * P + r] = 0.f;
+      __syncwarp();
+    }
+    const int r0s = cc.sub * S::ROWS;
+    const uint32_t um_stage = (S::ROWS == 64) ? (__shfl_sync(0xFFFFFFFFu, c.nwu, (r0s >> 5)) |
+                                                 __shfl_sync(0xFFFFFFFFu, c.nwu, (r0s >> 5) + 1))
+                                              : 1u;
+    if (!UNIFORM && !EXPORT && S::ROWS == 64 && r0s + 64 <= c.rows && um_stage == 0u) {
+      // stage fast path: 64 full rows, none in the fetch plan -> every row is T8 (or p = 0)
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+        base[jj] += 64 - __popc(ss[jj * 8 + (r0s >> 5)]) - __popc(ss[jj * 8 + (r0s >> 5) + 1]);
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        const int rl = 4 * q + r4;
+        const uint4 hv = *reinterpret_cast<const uint4*>(sd + rl * D + cg * 16);
+        uint32_t w[8];
+        t8_words16(hv, w);
+        float2 f[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
+#pragma unroll
+        for (int jj = 0; jj < HG; ++jj) {
+          const float pv = sp[jj * P + r0s + rl];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], pv, acc[jj][k]);
+        }
+      }
+    } else
 #pragma unroll(G == 1 ? S::ROWS / 16 : 1)
     for (int bb = 0; bb < S::ROWS / 16; ++bb) {
       const int b = cc.sub * (S::ROWS / 16) + bb;  // 16-row batch index inside the page
