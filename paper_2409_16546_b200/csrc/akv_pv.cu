@@ -288,14 +288,20 @@ template <int G, bool UNIFORM>
 struct Pv3Shape {
   static constexpr int HG = G < 4 ? G : 4;  // q-heads per pass (accumulator budget); passes re-read the page from L2
   static constexpr int NPASS = G / HG;
-  static constexpr int ROWS = UNIFORM ? 32 : 64;                 // rows per stage
+#ifndef AKV_PV_ROWS
+#define AKV_PV_ROWS 64
+#endif
+  static constexpr int ROWS = UNIFORM ? 32 : AKV_PV_ROWS;        // rows per stage
   static constexpr int HEAD = ROWS * D;                          // head bytes per stage
   static constexpr int NIB = UNIFORM ? ROWS * (D / 2) : 0;       // mid (= low) bytes per stage
   static constexpr int SLOT = HEAD + 2 * NIB;                    // 8 KB
   // per-page metadata (issued with the page's first stage): p[HG][P], sel[HG][8], need[G][2][8]
   static constexpr int M_P = 0, M_SEL = HG * P * 4, M_NEED = M_SEL + HG * 32;
   static constexpr int META = M_NEED + G * 64;
-  static constexpr int NS = 2;      // stages per warp ring (one in flight while one is computed)
+#ifndef AKV_PV_NS
+#define AKV_PV_NS 2
+#endif
+  static constexpr int NS = UNIFORM ? 2 : AKV_PV_NS;  // stages per warp ring (NS-1 in flight while one is computed)
   static constexpr int WARPS = 4;
   static constexpr int PER_WARP = NS * SLOT + 2 * META + NS * 8;
   static constexpr int SMEM = WARPS * PER_WARP;
@@ -492,16 +498,21 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
       __syncwarp();
     }
     const int r0s = cc.sub * S::ROWS;
-    const uint32_t um_stage = (S::ROWS == 64) ? (__shfl_sync(0xFFFFFFFFu, c.nwu, (r0s >> 5)) |
-                                                 __shfl_sync(0xFFFFFFFFu, c.nwu, (r0s >> 5) + 1))
-                                              : 1u;
-    if (!UNIFORM && !EXPORT && S::ROWS == 64 && r0s + 64 <= c.rows && um_stage == 0u) {
-      // stage fast path: 64 full rows, none in the fetch plan -> every row is T8 (or p = 0)
+    constexpr int SW = S::ROWS / 32;  // 32-row chunks per stage
+    uint32_t um_stage = 0u;
 #pragma unroll
-      for (int jj = 0; jj < HG; ++jj)
-        base[jj] += 64 - __popc(ss[jj * 8 + (r0s >> 5)]) - __popc(ss[jj * 8 + (r0s >> 5) + 1]);
+    for (int w = 0; w < SW; ++w) um_stage |= __shfl_sync(0xFFFFFFFFu, c.nwu, (r0s >> 5) + w);
+    if (!UNIFORM && !EXPORT && r0s + S::ROWS <= c.rows && um_stage == 0u) {
+      // stage fast path: full rows, none in the fetch plan -> every row is T8 (or p = 0)
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        int ns = 0;
+#pragma unroll
+        for (int w = 0; w < SW; ++w) ns += __popc(ss[jj * 8 + (r0s >> 5) + w]);
+        base[jj] += S::ROWS - ns;
+      }
 #pragma unroll 4
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < S::ROWS / 4; ++q) {
         const int rl = 4 * q + r4;
         const uint4 hv = *reinterpret_cast<const uint4*>(sd + rl * D + cg * 16);
         uint32_t w[8];
