@@ -12,9 +12,6 @@ import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libakv.so")
-# measurement aid: tools/build_probe.sh variants (never set in tests / bench runs that report numbers)
-if os.environ.get("AKV_LIB_PROBE"):
-    LIB_PATH = os.environ["AKV_LIB_PROBE"]
 
 HEAD_DIM = 128
 PAGE_TOKENS = 256

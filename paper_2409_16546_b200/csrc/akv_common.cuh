@@ -7,9 +7,6 @@
 
 #include "akv.h"
 
-#ifndef AKV_PROBE
-#define AKV_PROBE 0  // measurement-aid builds only (tools/build_probe.sh); 0 in libakv.so
-#endif
 
 namespace akv {
 
