@@ -286,7 +286,7 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
 // ---------------------------------------------------------------------------
 template <int G, bool UNIFORM>
 struct Pv3Shape {
-  static constexpr int HG = G < 4 ? G : 4;  // q-heads per pass (accumulator budget); passes re-read the page from L2
+  static constexpr int HG = G < 4 ? G : (UNIFORM ? 4 : 2);  // q-heads per pass (registers); passes re-read the page from L2
   static constexpr int NPASS = G / HG;
 #ifndef AKV_PV_ROWS
 #define AKV_PV_ROWS 64
