@@ -57,14 +57,34 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
   const int nch = (n + 31) / 32;  // 32-token chunks with (max, sum exp) from the QK kernel
   __shared__ SelSmem sm;
 
-  // 1. global softmax statistics (fixed assignment + butterfly: deterministic)
+  // the first batch of scores is loaded before the statistics are known (overlaps step 1)
+  constexpr int BT = 8;
+  const float* sc = st.scores + (size_t)h * cap;
+  float sv0[BT];
+#pragma unroll
+  for (int b = 0; b < BT; ++b) {
+    const int t = b * ST + tid;
+    sv0[b] = t < n ? sc[t] : 0.f;
+  }
+
+  // 1. global softmax statistics (fixed assignment + butterfly: deterministic); the
+  //    chunk pairs are read once (up to 8 per lane) and reused for the second pass
   if (warp == 0) {
     const float2* ps = reinterpret_cast<const float2*>(st.page_stats) + (size_t)h * s.max_pages * (P / 32);
+    constexpr int CR = 8;
+    float2 cv[CR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) cv[r] = lane + 32 * r < nch ? ps[lane + 32 * r] : make_float2(-INFINITY, 0.f);
     float m = -INFINITY;
-    for (int i = lane; i < nch; i += 32) m = fmaxf(m, ps[i].x);
+#pragma unroll
+    for (int r = 0; r < CR; ++r) m = fmaxf(m, cv[r].x);
+    for (int i = lane + 32 * CR; i < nch; i += 32) m = fmaxf(m, ps[i].x);
     m = warp_max(m);
     float l = 0.f;
-    for (int i = lane; i < nch; i += 32) {
+#pragma unroll
+    for (int r = 0; r < CR; ++r)
+      if (lane + 32 * r < nch) l += cv[r].y * expf(cv[r].x - m);
+    for (int i = lane + 32 * CR; i < nch; i += 32) {
       const float2 v = ps[i];
       l += v.y * expf(v.x - m);
     }
@@ -84,18 +104,16 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
   const float invL = 1.0f / L;
   const bool est = cfg.force_tier == 0 && cfg.trunc_bits == 0 && cfg.k_sel > 0;  // k_sel = 0: softmax only
   const int k_sel = max(min(cfg.k_sel, AKV_MAX_KSEL), 1);
-  const float* sc = st.scores + (size_t)h * cap;
   float* pr = st.probs + (size_t)h * cap;
   uint32_t* bits = st.sel_bits + (size_t)h * (cap >> 5);
 
   // 2. probabilities, bitmap reset, candidate compaction (loads batched BT deep)
-  constexpr int BT = 8;
   for (int t0 = 0; t0 < n; t0 += ST * BT) {
     float sv[BT];
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
       const int t = t0 + b * ST + tid;
-      sv[b] = t < n ? sc[t] : 0.f;
+      sv[b] = t0 == 0 ? sv0[b] : (t < n ? sc[t] : 0.f);
     }
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
