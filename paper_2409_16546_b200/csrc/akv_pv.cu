@@ -303,7 +303,7 @@ struct Pv3Shape {
 #endif
   static constexpr int NS = UNIFORM ? 2 : AKV_PV_NS;  // stages per warp ring (NS-1 in flight while one is computed)
   static constexpr int WARPS = 4;
-  static constexpr int PER_WARP = NS * SLOT + 2 * META + NS * 8;
+  static constexpr int PER_WARP = (NS * SLOT + 2 * META + NS * 8 + 127) & ~127;  // bulk-copy destinations stay 16 B aligned
   static constexpr int SMEM = WARPS * PER_WARP;
   static constexpr int MINB = G == 1 ? 3 : 2;
 };
