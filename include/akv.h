@@ -43,7 +43,6 @@ extern "C" {
 #define AKV_PAGE_LOW_OFF 49152
 #define AKV_MAX_GROUP 8       /* q heads per kv head */
 #define AKV_MAX_KSEL 64
-#define AKV_PAGES_PER_CTA 4   /* split-K granularity of the PV partials */
 
 enum {
   AKV_OK = 0,

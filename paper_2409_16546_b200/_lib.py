@@ -18,7 +18,6 @@ PAGE_TOKENS = 256
 PAGE_BYTES = 65536
 MAX_GROUP = 8
 MAX_KSEL = 64
-PAGES_PER_CTA = 4
 TARGET_UNKNOWN = -(1 << 31)
 
 AKV_OK, AKV_EINVAL, AKV_EUNSUPPORTED, AKV_ECUDA = 0, -1, -2, -3

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from paper_2409_16546_b200 import _lib
-from paper_2409_16546_b200._lib import HEAD_DIM, MAX_KSEL, PAGE_TOKENS, PAGES_PER_CTA, TARGET_UNKNOWN
+from paper_2409_16546_b200._lib import HEAD_DIM, MAX_KSEL, PAGE_TOKENS, TARGET_UNKNOWN
 from paper_2409_16546_b200.align_core import AlignConfig, DegenerateInputError, Tier
 from paper_2409_16546_b200.kv_store import AccessCounter, KVStore, _as_bits, decode_status
 

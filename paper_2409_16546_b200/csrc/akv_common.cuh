@@ -15,7 +15,6 @@ constexpr int P = AKV_PAGE_TOKENS;
 constexpr int PAGE = AKV_PAGE_BYTES;
 constexpr int MID = AKV_PAGE_MID_OFF;
 constexpr int LOW = AKV_PAGE_LOW_OFF;
-constexpr int PPC = AKV_PAGES_PER_CTA;
 
 // fp16 pattern helpers -------------------------------------------------------
 __device__ __forceinline__ int bexp16(uint32_t w) { return (w >> 10) & 0x1F; }
@@ -92,11 +91,6 @@ __device__ __forceinline__ uint4 ld_stream_u128(const void* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return r;
 }
-__device__ __forceinline__ uint32_t ld_stream_u32(const void* p, uint64_t pol) {
-  uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
-  return r;
-}
 
 // ---------------------------------------------------------------------------
 // mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
@@ -108,9 +102,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -139,41 +130,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-// 16-byte cp.async (LDGSTS, L2 only) and its completion as an mbarrier arrival.
-// The arrival does not increment the pending count (.noinc): the barrier's
-// init count includes one arrival per producer lane.
+// 16-byte cp.async (LDGSTS, L2 only).
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Copy the rows of a plane whose bit is set in an NW-word mask: ROW bytes per
-// row (ROW/16 lanes per row, 512/ROW rows per warp instruction); groups of rows
-// with no bit set are skipped (warp-uniform).
-template <int NW, int ROW>
-__device__ __forceinline__ void cp_rows(const uint32_t (&mk)[NW], uint8_t* dst, const uint8_t* src) {
-  constexpr int LPR = ROW / 16, RPI = 32 / LPR;  // lanes per row, rows per instruction
-  const int lane = threadIdx.x & 31;
-  const int rsub = lane / LPR, chunk = lane % LPR;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const uint32_t m = mk[w];
-    if (!m) continue;
-#pragma unroll
-    for (int g = 0; g < 32 / RPI; ++g) {
-      const uint32_t grpbits = (m >> (g * RPI)) & ((RPI == 32) ? 0xFFFFFFFFu : ((1u << RPI) - 1u));
-      if (!grpbits) continue;
-      const int r = w * 32 + g * RPI + rsub;
-      if ((grpbits >> rsub) & 1u) cp_async16(dst + r * ROW + chunk * 16, src + r * ROW + chunk * 16);
-    }
-  }
-}
 
-// Named barrier over `count` threads (ids 1.. are free; 0 is __syncthreads).
-__device__ __forceinline__ void named_bar(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 
 __device__ __forceinline__ float2 half2_bits_to_float2(uint32_t w) {
   __half2 h = *reinterpret_cast<__half2*>(&w);
@@ -204,11 +165,6 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 __device__ __forceinline__ int warp_sum_i(int v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-  return v;
-}
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;
