@@ -72,7 +72,7 @@ struct VRowP {
 // nibble rows fetched here.  Rare on the hot path, so kept out of line (I-cache).
 template <int G, int HG, bool EXPORT>
 __device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c, int b, int j0, akv_cfg_t cfg,
-                                                   const akv_step_t* stp, VRowP<HG> p, uint32_t um) {
+                                                   const akv_step_t* stp, VRowP<HG> p, uint32_t um, uint32_t qmask) {
   const akv_step_t& st = *stp;
   const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
   const int ch = b >> 1, sh16 = 16 * (b & 1);
@@ -91,6 +91,7 @@ __device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c,
   const uint64_t pol = evict_first_policy();
 #pragma unroll 1
   for (int i = 0; i < 4; ++i) {
+    if (!((qmask >> i) & 1u)) continue;  // quad handled by the caller's T8 path
     const int rr = 4 * i + r4, row = 16 * b + rr;
     const bool valid = rr < nvalid;
     const uint4 hv = i == 0 ? X.h[0] : (i == 1 ? X.h[1] : (i == 2 ? X.h[2] : X.h[3]));
@@ -260,7 +261,38 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
     return;
   }
   if constexpr (!UNIFORM) {
-    const VGen<HG> gen = v_generic_aligned<G, HG, EXPORT>(X, c, b, j0, cfg, &st, p, um);
+    // quads (4 rows) with no row in the fetch plan take the T8 path inline; the rest go
+    // through the out-of-line per-element rule
+    uint32_t gq = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if ((um >> (sh16 + 4 * i)) & 0xFu & (vmask16 >> (4 * i))) gq |= 1u << i;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if ((gq >> i) & 1u) continue;
+      uint32_t w[8];
+      t8_words16(X.h[i], w);
+      float2 f[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], p.v[jj][i], acc[jj][k]);
+      if (EXPORT && vt) {
+        const int rr = 4 * i + r4;
+        if (rr < nvalid) {
+#pragma unroll
+          for (int jj = 0; jj < HG; ++jj) {
+            const bool sel = (X.sel[jj] >> (sh16 + rr)) & 1u;
+            const uint32_t cd = sel ? 0x10101010u : 0x08080808u;
+            *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) = make_uint4(cd, cd, cd, cd);
+          }
+        }
+      }
+    }
+    if (!gq) return;
+    const VGen<HG> gen = v_generic_aligned<G, HG, EXPORT>(X, c, b, j0, cfg, &st, p, um, gq);
 #pragma unroll
     for (int jj = 0; jj < HG; ++jj) {
 #pragma unroll
