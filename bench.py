@@ -129,7 +129,7 @@ def reference_main(args):
 # clocks sampler
 # ---------------------------------------------------------------------------
 class Clocks:
-    """SM clock + throttle reasons sampled through NVML every ~2 ms in a thread
+    """SM clock + throttle reasons sampled through NVML every ~0.2 ms in a thread
     while the timed region runs (nvidia-smi's 100 ms loop is too coarse for a
     few-ms region); falls back to one nvidia-smi query when NVML is absent."""
 
@@ -172,7 +172,7 @@ class Clocks:
                 self._sample()
             except Exception:
                 return
-            time.sleep(0.002)
+            time.sleep(0.0002)
 
     def stop(self):
         self.stop_ev.set()
