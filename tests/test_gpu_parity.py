@@ -325,3 +325,8 @@ def test_decode_graph_copy_modes(zin, zout):
     dg = AD.DecodeGraph(b, g, rewind_to=n - 1, zero_copy_in=zin, zero_copy_out=zout).capture()
     out = dg.step(q, kt[:, :, n - 1], vt[:, :, n - 1])
     assert torch.equal(out, ref.o.cpu())
+
+
+def test_long_context_beyond_register_page_table():
+    """n = 33000 tokens = 129 pages: pages >= 128 take the page-table fallback path."""
+    _compare_case(Case(B=1, Hkv=1, g=1, n=33000, seed=123))
