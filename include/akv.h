@@ -110,15 +110,15 @@ typedef struct {
   int64_t* status;      /* [U*g] */
   uint8_t* k_tiers;     /* [U*g][d] read-bit codes 0/8/12/16 (out) */
   uint8_t* v_tiers;     /* [U*g][cap][d] or NULL: per-element V codes (debug/parity) */
-  uint32_t* work;       /* [8] persistent-kernel work queues; zero before first use, self-resetting */
+  uint32_t* work;       /* [8] reserved scratch (kept zero); the kernels use static work splits */
   uint32_t* need_bits;  /* [U*g][2][cap/32] V rows needing the mid / low nibble row (superset rule) */
 } akv_step_t;
 
 int akv_version(void);
 
 /* Bytes of one contiguous workspace that akv_step_carve() splits into every
- * akv_step_t buffer except q, o and v_tiers.  The workspace must be zeroed
- * once before its first use (the work queues inside reset themselves). */
+ * akv_step_t buffer except q, o and v_tiers.  Zero it once before its first
+ * use (every per-step buffer is fully rewritten by the kernels each step). */
 int64_t akv_workspace_bytes(int32_t n_units, int32_t group, int32_t max_pages);
 int akv_step_carve(akv_step_t* step, void* workspace, int32_t n_units, int32_t group, int32_t max_pages);
 
