@@ -39,7 +39,7 @@ class DecodeWorkspace:
         U, mp, d, dev = store.n_units, store.max_pages, store.n_dims, store.device
         H = U * group
         nbytes = int(L.akv_workspace_bytes(U, group, mp))
-        self.ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=dev)  # work queues start at 0
+        self.ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=dev)  # zeroed once (akv.h)
         base = (self.ws.data_ptr() + 255) & ~255
         self.step = _lib.AkvStep()
         _lib.check(L.akv_step_carve(ctypes.byref(self.step), base, U, group, mp), "akv_step_carve")
