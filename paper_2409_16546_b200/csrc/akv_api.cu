@@ -3,7 +3,7 @@
 
 namespace akv {
 void launch_qk(const akv_store_t&, const akv_cfg_t&, const akv_step_t&, int, cudaStream_t);
-void launch_select(const akv_store_t&, const akv_cfg_t&, const akv_step_t&, cudaStream_t);
+void launch_select(const akv_store_t&, const akv_cfg_t&, const akv_step_t&, int, cudaStream_t);
 void launch_pv(const akv_store_t&, const akv_cfg_t&, const akv_step_t&, int, cudaStream_t);
 void launch_combine(const akv_store_t&, const akv_cfg_t&, const akv_step_t&, cudaStream_t);
 
@@ -135,7 +135,7 @@ extern "C" int akv_softmax_select(const akv_store_t* s, const akv_cfg_t* c, cons
   int e = check(s, c, st);
   if (e) return e;
   if (max_len <= 0 || s->n_units == 0) return AKV_OK;
-  launch_select(*s, *c, *st, (cudaStream_t)stream);
+  launch_select(*s, *c, *st, max_len, (cudaStream_t)stream);
   return last_error();
 }
 
@@ -164,7 +164,7 @@ extern "C" int akv_decode_step(const akv_store_t* s, const akv_cfg_t* c, const a
   if (max_len <= 0 || s->n_units == 0) return AKV_OK;
   cudaStream_t cs = (cudaStream_t)stream;
   launch_qk(*s, *c, *st, max_len, cs);
-  launch_select(*s, *c, *st, cs);
+  launch_select(*s, *c, *st, max_len, cs);
   launch_pv(*s, *c, *st, max_len, cs);
   launch_combine(*s, *c, *st, cs);
   return last_error();

@@ -17,21 +17,22 @@
 
 namespace akv {
 
-constexpr int ST = 256;    // threads per select CTA
+constexpr int SW = 8;      // warps that run the digit scan and the o_est gather (fixed: results independent of ST)
 constexpr int CAND = 2048; // shared candidate capacity (overflow -> global fallback scan)
 
+template <int ST>
 struct SelSmem {
   unsigned hist[256];
   int cand_t[CAND];
   float cand_p[CAND];
   int sel[AKV_MAX_KSEL];
   int sel_sorted[AKV_MAX_KSEL];
-  float part[ST / 32][D];
+  float part[SW][D];
   float M, L;
   int ncand, nsel, need_eq, neq;
   unsigned vstar;
-  unsigned wsum[ST / 32];
-  int wfirst[ST / 32];
+  unsigned wsum[SW];
+  int wfirst[SW];
   int sel_page[AKV_MAX_KSEL];
   int tmin[4], tunk[4];
 };
@@ -46,7 +47,9 @@ __device__ __forceinline__ uint32_t v_word_exact(const uint8_t* vp, int tt, int 
   return (head << 8) | (mid << 4) | low;
 }
 
-__global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap) {
+template <int ST>
+__global__ void __launch_bounds__(ST, ST == 256 ? 4 : 1) select_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st,
+                                                                    int cap) {
   pdl_trigger();
   pdl_wait();
   const int h = blockIdx.x;
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = s.lengths[u];
   const int nch = (n + 31) / 32;  // 32-token chunks with (max, sum exp) from the QK kernel
-  __shared__ SelSmem sm;
+  __shared__ SelSmem<ST> sm;
 
   // the first batch of scores is loaded before the statistics are known (overlaps step 1)
   constexpr int BT = 8;
@@ -173,26 +176,28 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
         __syncthreads();
         {
           // digit of the k-th largest key: scan the histogram from the top bin down
-          // (thread t owns bin 255 - t; block-wide inclusive scan by warp shuffles)
-          const unsigned hv = sm.hist[255 - tid];
+          // (threads 0..255: thread t owns bin 255 - t; block-wide scan by warp shuffles)
+          const bool scan = tid < 256;
+          const unsigned hv = scan ? sm.hist[255 - tid] : 0u;
           unsigned incl = hv;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
             if (lane >= o) incl += y;
           }
-          if (lane == 31) sm.wsum[warp] = incl;
+          if (scan && lane == 31) sm.wsum[warp] = incl;
           __syncthreads();
           unsigned before = 0;
-          for (int w = 0; w < warp; ++w) before += sm.wsum[w];
+          if (scan)
+            for (int w = 0; w < warp; ++w) before += sm.wsum[w];
           incl += before;
-          const bool hit = (int)incl >= k || tid == 255;
+          const bool hit = scan && ((int)incl >= k || tid == 255);
           const unsigned hb = __ballot_sync(0xFFFFFFFFu, hit);
-          if (lane == 0) sm.wfirst[warp] = hb ? warp * 32 + __ffs(hb) - 1 : 0x7FFFFFFF;
+          if (scan && lane == 0) sm.wfirst[warp] = hb ? warp * 32 + __ffs(hb) - 1 : 0x7FFFFFFF;
           __syncthreads();
           int first = 0x7FFFFFFF;
 #pragma unroll
-          for (int w = 0; w < ST / 32; ++w) first = min(first, sm.wfirst[w]);
+          for (int w = 0; w < SW; ++w) first = min(first, sm.wfirst[w]);
           if (tid == first) {
             sm.need_eq = k - (int)(incl - hv);
             sm.vstar = prefix | ((unsigned)(255 - tid) << shift);
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
         k = sm.need_eq;
         prefix = sm.vstar;
         mask |= 0xFFu << shift;
-        sm.hist[tid] = 0;
+        if (tid < 256) sm.hist[tid] = 0;
         __syncthreads();
       }
       const unsigned vstar = sm.vstar;
@@ -268,12 +273,12 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
   {
     constexpr int RW = 4;  // rows loaded together (per warp: rows warp + 8r)
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int r0 = 0; warp + r0 * (ST / 32) < cnt; r0 += RW) {
+    for (int r0 = 0; warp < SW && warp + r0 * SW < cnt; r0 += RW) {
       float pv[RW];
       uint32_t wv[RW][4];
 #pragma unroll
       for (int r = 0; r < RW; ++r) {
-        const int i = warp + (r0 + r) * (ST / 32);
+        const int i = warp + (r0 + r) * SW;
         pv[r] = 0.f;
         wv[r][0] = wv[r][1] = wv[r][2] = wv[r][3] = 0u;
         if (i < cnt) {
@@ -286,22 +291,24 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
       }
 #pragma unroll
       for (int r = 0; r < RW; ++r) {
-        if (warp + (r0 + r) * (ST / 32) < cnt) {
+        if (warp + (r0 + r) * SW < cnt) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             acc[e] = fmaf(pv[r], __half2float(__ushort_as_half((unsigned short)wv[r][e])), acc[e]);
         }
       }
     }
+    if (warp < SW) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) sm.part[warp][lane * 4 + e] = acc[e];
+      for (int e = 0; e < 4; ++e) sm.part[warp][lane * 4 + e] = acc[e];
+    }
   }
   __syncthreads();
   if (tid < D) {
     const int r = tid;
     float o = 0.f;
 #pragma unroll
-    for (int w = 0; w < ST / 32; ++w) o += sm.part[w][r];
+    for (int w = 0; w < SW; ++w) o += sm.part[w][r];
     st.o_est[(size_t)h * D + r] = o;
     const bool known = o != 0.f;
     const int tg = known ? floor_log2f(o) - 10 : AKV_TARGET_UNKNOWN;
@@ -391,9 +398,13 @@ __global__ void __launch_bounds__(ST, 4) select_kernel(akv_store_t s, akv_cfg_t 
   }
 }
 
-void launch_select(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, cudaStream_t stream) {
+void launch_select(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len, cudaStream_t stream) {
   const int cap = s.max_pages * P;
-  launch_pdl(select_kernel, dim3(s.n_units * cfg.group), dim3(ST), 0, stream, s, cfg, st, cap);
+  // long contexts: more threads per head (the per-head chain is the latency)
+  if (max_len > 8192)
+    launch_pdl(select_kernel<1024>, dim3(s.n_units * cfg.group), dim3(1024), 0, stream, s, cfg, st, cap);
+  else
+    launch_pdl(select_kernel<256>, dim3(s.n_units * cfg.group), dim3(256), 0, stream, s, cfg, st, cap);
 }
 
 }  // namespace akv
