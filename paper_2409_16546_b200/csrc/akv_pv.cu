@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
 }
 
 // o = o_est + sum over the unit's pages of o_partial, fixed order (deterministic):
-// groups of four pages, then the rest.  All partials of a 16-page window are
+// groups of four pages, then the rest.  All partials of a 32-page window are
 // loaded before they are summed (one memory round trip per window).
 __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st) {
   pdl_trigger();
@@ -632,20 +632,21 @@ __global__ void __launch_bounds__(128) combine_kernel(akv_store_t s, akv_cfg_t c
   const int npg = (n + P - 1) / P;
   const float* part = st.o_partial + (size_t)h * s.max_pages * D + threadIdx.x;
   float acc = st.o_est[(size_t)h * D + threadIdx.x];
-  for (int w0 = 0; w0 < npg; w0 += 16) {
-    float v[16];
+  constexpr int WIN = 32;
+  for (int w0 = 0; w0 < npg; w0 += WIN) {
+    float v[WIN];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = w0 + i < npg ? part[(w0 + i) * D] : 0.f;
-    const int m = min(npg - w0, 16);
+    for (int i = 0; i < WIN; ++i) v[i] = w0 + i < npg ? part[(w0 + i) * D] : 0.f;
+    const int m = min(npg - w0, WIN);
     int i = 0;
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int g = 0; g < WIN / 4; ++g)
       if (i + 4 <= m) {
         acc += ((v[4 * g] + v[4 * g + 1]) + (v[4 * g + 2] + v[4 * g + 3]));
         i += 4;
       }
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < WIN; ++r)
       if (r >= i && r < m) acc += v[r];
   }
   st.o[(size_t)h * D + threadIdx.x] = acc;
