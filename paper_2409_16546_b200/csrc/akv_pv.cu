@@ -67,27 +67,114 @@ struct VRowP {
   float v[HG][4];
 };
 
-// Aligned rows of a batch in the union fetch plan: per q-head mode (selected -> skip,
-// no need bit -> T8, row strategy -> row tier, element strategy -> per-element rule D4),
-// nibble rows fetched here.  Rare on the hot path, so kept out of line (I-cache).
+// One aligned row in the union fetch plan (this lane's 16 channels): per q-head mode
+// (selected -> skip, no need bit -> T8, row strategy -> row tier, element strategy ->
+// per-element rule D4) applied to the fetched nibbles; contributions into out.
+// selw[jj]: the row's 32-row selection word; vt_row: export pointer of the row (or null).
 template <int G, int HG, bool EXPORT>
-__device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c, int b, int j0, akv_cfg_t cfg,
-                                                   const akv_step_t* stp, VRowP<HG> p, uint32_t um, uint32_t qmask) {
-  const akv_step_t& st = *stp;
-  const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
-  const int ch = b >> 1, sh16 = 16 * (b & 1);
-  const int nvalid = min(max(c.rows - 16 * b, 0), 16);
-  const int capw = c.cap >> 5;
-  VGen<HG> out;
+__device__ __forceinline__ void v_row_generic(VGen<HG>& out, const uint4& hv, uint2 mw, uint2 lw, int row, bool valid,
+                                              const PvCtx& c, int j0, const akv_cfg_t& cfg, const akv_step_t& st,
+                                              const float (&pvj)[HG], const uint32_t (&selw)[HG], uint8_t* vt_row) {
+  const int lane = threadIdx.x & 31, cg = lane & 7;
+  const int capw = c.cap >> 5, ch = row >> 5;
+#pragma unroll
+  for (int jj = 0; jj < HG; ++jj) {
+    const size_t h = (size_t)c.u * G + j0 + jj;
+    const float pv = pvj[jj];
+    int mode;  // 0 skip, 1 element, 8/12/16 tier
+    if ((selw[jj] >> (row & 31)) & 1u) {
+      mode = 0;
+    } else {
+      const uint32_t nm = st.need_bits[h * 2 * capw + c.pg * 8 + ch];
+      if (!((nm >> (row & 31)) & 1u)) {
+        mode = 8;  // includes p == 0 (D5)
+      } else if (cfg.strategy == 1) {
+        const uint32_t nl = st.need_bits[h * 2 * capw + capw + c.pg * 8 + ch];
+        mode = ((nl >> (row & 31)) & 1u) ? 16 : 12;
+      } else {
+        mode = 1;
+      }
+    }
+    if (!valid) mode = 0;
+    uint32_t w[8];
+    uint32_t cds[4] = {0u, 0u, 0u, 0u};
+    if (mode == 0) {
+      if (EXPORT && vt_row && valid)
+        *reinterpret_cast<uint4*>(vt_row + (size_t)(j0 + jj) * c.cap * D) =
+            make_uint4(0x10101010u, 0x10101010u, 0x10101010u, 0x10101010u);
+      continue;
+    }
+    if (mode == 8) {
+      t8_words16(hv, w);
+      if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = 0x08080808u;
+    } else if (mode != 1) {
+      const TierMask tm = tier_mask(mode);
+      assemble8(hv.x, hv.y, bsel(tm.mk, mw.x, 0x88888888u), bsel(tm.lk, lw.x, tm.lf), w);
+      assemble8(hv.z, hv.w, bsel(tm.mk, mw.y, 0x88888888u), bsel(tm.lk, lw.y, tm.lf), w + 4);
+      out.adj[jj][0] -= 16;
+      out.adj[jj][mode == 12 ? 1 : 2] += 16;
+      if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = (uint32_t)mode * 0x01010101u;
+    } else {
+      assemble8(hv.x, hv.y, mw.x, lw.x, w);
+      assemble8(hv.z, hv.w, mw.y, lw.y, w + 4);
+      const int ep = pv > 0.f ? floor_log2f(pv) : -30000;
+      const int4* tp = reinterpret_cast<const int4*>(st.targets + h * D + cg * 16);
+      int tg[16];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int4 t = tp[q4];
+        tg[4 * q4] = t.x;
+        tg[4 * q4 + 1] = t.y;
+        tg[4 * q4 + 2] = t.z;
+        tg[4 * q4 + 3] = t.w;
+      }
+      const uint32_t hb[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int g = tg[e] == AKV_TARGET_UNKNOWN ? -(1 << 20) : 17 + tg[e] - cfg.margin_bits;
+        const uint32_t hbyte = (hb[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+        const int E = max((int)((hbyte >> 2) & 31u), 1) + ep;
+        const bool km = E > g, kl = E > g + 4;
+        const int sh = 16 * (e & 1);
+        uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
+        w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
+        w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
+        out.adj[jj][0] -= km ? 1 : 0;
+        out.adj[jj][1] += (km && !kl) ? 1 : 0;
+        out.adj[jj][2] += kl ? 1 : 0;
+        if (EXPORT) cds[e >> 2] |= (kl ? 16u : (km ? 12u : 8u)) << (8 * (e & 3));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out.acc[jj][k] = ffma2_scalar(half2_bits_to_float2(w[k]), pv, out.acc[jj][k]);
+    if (EXPORT && vt_row)
+      *reinterpret_cast<uint4*>(vt_row + (size_t)(j0 + jj) * c.cap * D) = make_uint4(cds[0], cds[1], cds[2], cds[3]);
+  }
+}
+
+template <int HG>
+__device__ __forceinline__ void vgen_zero(VGen<HG>& out) {
 #pragma unroll
   for (int jj = 0; jj < HG; ++jj) {
     out.adj[jj][0] = out.adj[jj][1] = out.adj[jj][2] = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) out.acc[jj][q] = make_float2(0.f, 0.f);
   }
+}
+
+// Aligned rows of a batch in the union fetch plan (quads in qmask), nibble rows fetched
+// here.  Rare on the hot path, so kept out of line (I-cache).
+template <int G, int HG, bool EXPORT>
+__device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c, int b, int j0, akv_cfg_t cfg,
+                                                   const akv_step_t* stp, VRowP<HG> p, uint32_t um, uint32_t qmask) {
+  const akv_step_t& st = *stp;
+  const int lane = threadIdx.x & 31, r4 = lane >> 3, cg = lane & 7;
+  const int nvalid = min(max(c.rows - 16 * b, 0), 16);
+  VGen<HG> out;
+  vgen_zero(out);
   uint8_t* vt = nullptr;
   if (EXPORT && st.v_tiers) vt = st.v_tiers + ((size_t)c.u * G * c.cap + (size_t)c.pg * P + 16 * b) * D + cg * 16;
-  const uint32_t ul = __shfl_sync(0xFFFFFFFFu, c.nwu, 8 + ch);
+  const uint32_t ul = __shfl_sync(0xFFFFFFFFu, c.nwu, 8 + (b >> 1));
   const uint64_t pol = evict_first_policy();
 #pragma unroll 1
   for (int i = 0; i < 4; ++i) {
@@ -98,81 +185,40 @@ __device__ __noinline__ VGen<HG> v_generic_aligned(VBatch<HG, false> X, PvCtx c,
     uint2 mw = make_uint2(0u, 0u), lw = make_uint2(0u, 0u);
     if (valid && ((um >> (row & 31)) & 1u)) mw = ld_stream_u64(c.vb + MID + row * (D / 2) + cg * 8, pol);
     if (valid && ((ul >> (row & 31)) & 1u)) lw = ld_stream_u64(c.vb + LOW + row * (D / 2) + cg * 8, pol);
+    float pvj[HG];
+    uint32_t selw[HG];
 #pragma unroll
     for (int jj = 0; jj < HG; ++jj) {
-      const size_t h = (size_t)c.u * G + j0 + jj;
-      const float pv = i == 0 ? p.v[jj][0] : (i == 1 ? p.v[jj][1] : (i == 2 ? p.v[jj][2] : p.v[jj][3]));
-      int mode;  // 0 skip, 1 element, 8/12/16 tier
-      if ((X.sel[jj] >> (sh16 + rr)) & 1u) {
-        mode = 0;
-      } else {
-        const uint32_t nm = st.need_bits[h * 2 * capw + c.pg * 8 + ch];
-        if (!((nm >> (row & 31)) & 1u)) {
-          mode = 8;  // includes p == 0 (D5)
-        } else if (cfg.strategy == 1) {
-          const uint32_t nl = st.need_bits[h * 2 * capw + capw + c.pg * 8 + ch];
-          mode = ((nl >> (row & 31)) & 1u) ? 16 : 12;
-        } else {
-          mode = 1;
-        }
-      }
-      if (!valid) mode = 0;
-      uint32_t w[8];
-      uint32_t cds[4] = {0u, 0u, 0u, 0u};
-      if (mode == 0) {
-        if (EXPORT && vt && valid)
-          *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) =
-              make_uint4(0x10101010u, 0x10101010u, 0x10101010u, 0x10101010u);
-        continue;
-      }
-      if (mode == 8) {
-        t8_words16(hv, w);
-        if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = 0x08080808u;
-      } else if (mode != 1) {
-        const TierMask tm = tier_mask(mode);
-        assemble8(hv.x, hv.y, bsel(tm.mk, mw.x, 0x88888888u), bsel(tm.lk, lw.x, tm.lf), w);
-        assemble8(hv.z, hv.w, bsel(tm.mk, mw.y, 0x88888888u), bsel(tm.lk, lw.y, tm.lf), w + 4);
-        out.adj[jj][0] -= 16;
-        out.adj[jj][mode == 12 ? 1 : 2] += 16;
-        if (EXPORT) cds[0] = cds[1] = cds[2] = cds[3] = (uint32_t)mode * 0x01010101u;
-      } else {
-        assemble8(hv.x, hv.y, mw.x, lw.x, w);
-        assemble8(hv.z, hv.w, mw.y, lw.y, w + 4);
-        const int ep = pv > 0.f ? floor_log2f(pv) : -30000;
-        const int4* tp = reinterpret_cast<const int4*>(st.targets + h * D + cg * 16);
-        int tg[16];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int4 t = tp[q4];
-          tg[4 * q4] = t.x;
-          tg[4 * q4 + 1] = t.y;
-          tg[4 * q4 + 2] = t.z;
-          tg[4 * q4 + 3] = t.w;
-        }
-        const uint32_t hb[4] = {hv.x, hv.y, hv.z, hv.w};
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int g = tg[e] == AKV_TARGET_UNKNOWN ? -(1 << 20) : 17 + tg[e] - cfg.margin_bits;
-          const uint32_t hbyte = (hb[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-          const int E = max((int)((hbyte >> 2) & 31u), 1) + ep;
-          const bool km = E > g, kl = E > g + 4;
-          const int sh = 16 * (e & 1);
-          uint32_t w16 = (w[e >> 1] >> sh) & 0xFFFFu;
-          w16 = kl ? w16 : (km ? ((w16 & 0xFFF0u) | 0x8u) : ((w16 & 0xFF00u) | 0x80u));
-          w[e >> 1] = (w[e >> 1] & ~(0xFFFFu << sh)) | (w16 << sh);
-          out.adj[jj][0] -= km ? 1 : 0;
-          out.adj[jj][1] += (km && !kl) ? 1 : 0;
-          out.adj[jj][2] += kl ? 1 : 0;
-          if (EXPORT) cds[e >> 2] |= (kl ? 16u : (km ? 12u : 8u)) << (8 * (e & 3));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) out.acc[jj][k] = ffma2_scalar(half2_bits_to_float2(w[k]), pv, out.acc[jj][k]);
-      if (EXPORT && vt)
-        *reinterpret_cast<uint4*>(vt + (size_t)(j0 + jj) * c.cap * D + (size_t)rr * D) =
-            make_uint4(cds[0], cds[1], cds[2], cds[3]);
+      pvj[jj] = i == 0 ? p.v[jj][0] : (i == 1 ? p.v[jj][1] : (i == 2 ? p.v[jj][2] : p.v[jj][3]));
+      selw[jj] = X.sel[jj];
     }
+    v_row_generic<G, HG, EXPORT>(out, hv, mw, lw, row, valid, c, j0, cfg, st, pvj, selw,
+                                 vt ? vt + (size_t)rr * D : nullptr);
   }
+  return out;
+}
+
+// One quad (this lane's row) of a wide-group stage in the fetch plan; out of line.
+template <int G, int HG>
+__device__ __noinline__ VGen<HG> v_quad_generic(uint4 hv, int row, bool valid, PvCtx c, int j0, akv_cfg_t cfg,
+                                                const akv_step_t* stp, VRowP<HG> p, const uint32_t* ss) {
+  const int lane = threadIdx.x & 31, cg = lane & 7;
+  VGen<HG> out;
+  vgen_zero(out);
+  const uint32_t um = __shfl_sync(0xFFFFFFFFu, c.nwu, row >> 5 & 7);
+  const uint32_t ul = __shfl_sync(0xFFFFFFFFu, c.nwu, 8 + ((row >> 5) & 7));
+  const uint64_t pol = evict_first_policy();
+  uint2 mw = make_uint2(0u, 0u), lw = make_uint2(0u, 0u);
+  if (valid && ((um >> (row & 31)) & 1u)) mw = ld_stream_u64(c.vb + MID + row * (D / 2) + cg * 8, pol);
+  if (valid && ((ul >> (row & 31)) & 1u)) lw = ld_stream_u64(c.vb + LOW + row * (D / 2) + cg * 8, pol);
+  float pvj[HG];
+  uint32_t selw[HG];
+#pragma unroll
+  for (int jj = 0; jj < HG; ++jj) {
+    pvj[jj] = p.v[jj][0];
+    selw[jj] = ss[jj * 8 + (row >> 5)];
+  }
+  v_row_generic<G, HG, false>(out, hv, mw, lw, row, valid, c, j0, cfg, *stp, pvj, selw, nullptr);
   return out;
 }
 
@@ -318,7 +364,7 @@ __device__ __forceinline__ void v_compute(const VBatch<HG, UNIFORM>& X, const Pv
 // ---------------------------------------------------------------------------
 template <int G, bool UNIFORM>
 struct Pv3Shape {
-  static constexpr int HG = G < 4 ? G : (UNIFORM ? 4 : 2);  // q-heads per pass (registers); passes re-read the page from L2
+  static constexpr int HG = G < 4 ? G : 4;  // q-heads per pass (accumulator budget); passes re-read the page from L2
   static constexpr int NPASS = G / HG;
 #ifndef AKV_PV_ROWS
 #define AKV_PV_ROWS 64
@@ -557,6 +603,61 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
           const float pv = sp[jj * P + r0s + rl];
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], pv, acc[jj][k]);
+        }
+      }
+    } else if (!UNIFORM && !EXPORT && G >= 4) {
+      // wide groups: 4-row quads; quads without rows in the fetch plan take the T8 path
+      // inline (p is pre-zeroed for selected rows / the page end), the rest go out of line
+      const int nvs = min(S::ROWS, c.rows - r0s);
+#pragma unroll
+      for (int jj = 0; jj < HG; ++jj) {
+        int ns = 0;
+#pragma unroll
+        for (int w = 0; w < SW; ++w) {
+          const int valid = min(max(nvs - 32 * w, 0), 32);
+          const uint32_t vm = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+          ns += __popc(ss[jj * 8 + (r0s >> 5) + w] & vm);
+        }
+        base[jj] += nvs - ns;
+      }
+#pragma unroll 1
+      for (int q = 0; 4 * q < nvs; ++q) {
+        const int rl = 4 * q + r4, row = r0s + rl;
+        const bool valid = rl < nvs;
+        const int qr = r0s + 4 * q;  // first row of the quad (quads never straddle a 32-row chunk)
+        const uint32_t fl = (__shfl_sync(0xFFFFFFFFu, c.nwu, qr >> 5) >> (qr & 31)) & 0xFu;
+        const uint4 hv = valid ? *reinterpret_cast<const uint4*>(sd + rl * D + cg * 16) : make_uint4(0u, 0u, 0u, 0u);
+        if (!fl) {
+          uint32_t w[8];
+          t8_words16(hv, w);
+          float2 f[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = half2_bits_to_float2(w[k]);
+#pragma unroll
+          for (int jj = 0; jj < HG; ++jj) {
+            const float pv = valid ? sp[jj * P + row] : 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[jj][k] = ffma2_scalar(f[k], pv, acc[jj][k]);
+          }
+        } else {
+          VRowP<HG> pq;
+#pragma unroll
+          for (int jj = 0; jj < HG; ++jj) {
+            pq.v[jj][0] = valid ? sp[jj * P + row] : 0.f;
+            pq.v[jj][1] = pq.v[jj][2] = pq.v[jj][3] = 0.f;
+          }
+          const VGen<HG> g = v_quad_generic<G, HG>(hv, row, valid, c, j0, cfg, &st, pq, ss);
+#pragma unroll
+          for (int jj = 0; jj < HG; ++jj) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              acc[jj][k].x += g.acc[jj][k].x;
+              acc[jj][k].y += g.acc[jj][k].y;
+            }
+            adj[jj][0] += g.adj[jj][0];
+            adj[jj][1] += g.adj[jj][1];
+            adj[jj][2] += g.adj[jj][2];
+          }
         }
       }
     } else
