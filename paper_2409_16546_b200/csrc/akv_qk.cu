@@ -1,4 +1,6 @@
 // scores_aligned for every (unit, q-head) of a batch.
+// Two kernels: qk_kernel below (G = 1, 2) and qk5_kernel (GQA groups G = 4, 8,
+// tensor cores; further down).
 //
 // Direct-load streaming kernel: every warp owns a contiguous range of
 // (unit, page) items (balanced split over all resident warps; no shared-memory
@@ -168,15 +170,18 @@ __device__ __forceinline__ void k_compute(const KBatch& X, const QkWarp<G>& ws, 
   }
 }
 
-// Rule 1 for unit u, all G heads; builds the warp's channel lists.
+// Rule 1 for unit u, all G heads: per-head channel codes (0 SKIP, 8, 12, 16),
+// their union over the group, and (book) the per-step bookkeeping.
 // Lane l owns channels l + 32k (k = 0..3).
 template <int G, bool TRUNC>
-__device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int u,
-                           int n, bool book) {
+__device__ __forceinline__ void k_rule1(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int u,
+                                        int n, bool book, uint32_t (&qw)[G][4], int (&code)[G][4],
+                                        int (&ucode)[4]) {
   const int lane = threadIdx.x & 31;
   const bool aligned = cfg.force_tier == 0 && !TRUNC;
-  uint32_t cm[4], qw[G][4];
-  int code[G][4], ucode[4] = {0, 0, 0, 0};
+  uint32_t cm[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ucode[k] = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) cm[k] = s.colmax[(size_t)u * D + lane + 32 * k] & 0x7FFFu;
 #pragma unroll
@@ -239,18 +244,39 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
       }
     }
   }
+  if (book) {
+    int n8 = 0, nf = 0, n16 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      n8 += __popc(__ballot_sync(0xFFFFFFFFu, ucode[k] == 8));
+      nf += __popc(__ballot_sync(0xFFFFFFFFu, ucode[k] >= 12));
+      n16 += __popc(__ballot_sync(0xFFFFFFFFu, ucode[k] == 16));
+    }
+    if (lane == 0) {
+      st.unit_bytes[(size_t)u * 4 + 0] = (int64_t)n * (n8 + nf) + (int64_t)(n / 2) * (nf + n16);
+      st.unit_bytes[(size_t)u * 4 + 1] = 0;
+    }
+  }
+}
+
+// Rule 1 + the warp's channel lists for the direct-load kernels.
+template <int G, bool TRUNC>
+__device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int u,
+                           int n, bool book) {
+  const int lane = threadIdx.x & 31;
+  uint32_t qw[G][4];
+  int code[G][4], ucode[4];
+  k_rule1<G, TRUNC>(s, cfg, st, u, n, book, qw, code, ucode);
   // lists: T8 class first, then T12/T16 (ascending channel inside each class)
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t b8[4], bf[4], b16[4];
-  int n8 = 0, nf = 0, n16 = 0;
+  uint32_t b8[4], bf[4];
+  int n8 = 0, nf = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     b8[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 8);
     bf[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
-    b16[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 16);
     n8 += __popc(b8[k]);
     nf += __popc(bf[k]);
-    n16 += __popc(b16[k]);
   }
   const int n8p = (n8 + 7) & ~7, nlp = n8p + ((nf + 7) & ~7);
   for (int i = lane; i < (D + 16) / 32 + 1; i += 32) ws.low[i] = 0u;
@@ -296,10 +322,6 @@ __device__ void k_prologue(QkWarp<G>& ws, const akv_store_t& s, const akv_cfg_t&
       ws.qrep[j][sl] = 0u;
       if (G > 1) ws.hm[j][sl] = make_uint2(0xFFFFFFFFu, 0u);
     }
-  }
-  if (book && lane == 0) {
-    st.unit_bytes[(size_t)u * 4 + 0] = (int64_t)n * (n8 + nf) + (int64_t)(n / 2) * (nf + n16);
-    st.unit_bytes[(size_t)u * 4 + 1] = 0;
   }
   if (lane == 0) {
     ws.n8p = n8p;
@@ -435,24 +457,52 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
 }
 
 // ---------------------------------------------------------------------------
-// qk v3: per-warp cp.async ring.  Each warp copies its 8-channel batches
-// (head rows, and the T12/T16 channels' mid / low rows) into a private ring of
-// NB shared-memory slots with 16-byte cp.async (one commit group per batch),
-// NB-1 batches ahead of the math, continuing across the pages of a unit; the
-// in-flight data lives in shared memory instead of registers, so more of it
-// fits.  The math reads the slot (LDS.128 / LDS.64) and reuses k_compute.
+// qk v5 (GQA groups, G = 4 / 8): tensor-core scores from a per-warp cp.async ring.
+//
+// The G q-heads of a unit share every K tile, so a page is a small GEMM:
+// scores[256 tokens][G] = K~^T[256][channels] x Q[channels][G], issued as
+// mma.sync m16n8k8 (fp16 in, fp32 accumulate: products exact, D9) with the
+// heads on N (G <= 8).  Per-head tiers differ per channel, so K~ is split by
+// tier variant: a chunk's words are rebuilt once at the union tier and masked
+// down to T12 / T8 (midpoint fill), and each variant is multiplied by the q
+// fragment that holds only the heads of that tier (zero elsewhere):
+//   s_j = sum_c q_jc K~_{tier_j(c)}(c) = sum_v K~_v . (q_j masked to tier v).
+// The channel order inside the reduction is free, so list positions map
+// straight onto the mma K index: lane (g, t) holds positions 2t, 2t+1 of an
+// 8-channel chunk for tokens 16g..16g+15 and 128+16g..+15; m16 tile i < 8
+// takes tokens 16g+2i (row g) and 16g+2i+1 (row g+8) of the first page half,
+// tiles 8..15 the same in the second half.
+//
+// With the math this light the kernel is bound by how many bytes are in
+// flight (DRAM latency under load is several us), so the rows are staged by
+// 16-byte cp.async into a ring of 4 KB slots per warp, NB-1 slots ahead of the
+// math and continuous across the pages of a unit: a slot is 16 T8-class head
+// rows, or 8 T12/T16-class head rows + their mid rows (+ low rows for T16).
+// Shared-memory reads are bank-conflict free: head rows are read as 4 rows x
+// 128 B per LDS.128; the 128 B nibble rows are stored with their 64 B halves
+// swapped on every other row pair.
 // ---------------------------------------------------------------------------
-constexpr int Q3_SLOT = 4096;  // 8 channels: head [8][256 B] | mid [8][128 B] | low [8][128 B]
+constexpr int Q5_SLOT = 4096;
+constexpr int Q5_CHUNKS = 18;  // (128 + 15 + 7) / 8 eight-channel chunks: T8 class padded to 16, T12/T16 class to 8
 
 template <int G>
-struct Qk3Shape {
-  static constexpr int HG = G < 4 ? G : 4;
-  static constexpr int NB = 4;  // ring slots per warp
+struct alignas(16) Qk5Warp {
+  uint32_t off[Q5_CHUNKS * 8];            // list position -> channel * P
+  uint32_t bf[Q5_CHUNKS][3][32];          // per chunk, tier variant (T8, T12, T16), lane: the B fragment
+  uint32_t low[(Q5_CHUNKS * 8 + 31) / 32];  // list position bitmask: low row needed (T16 in the union)
+  uint8_t vmask[Q5_CHUNKS];               // variants present per chunk (bit 0 T8, 1 T12, 2 T16)
+  int n8p, nlp, unit, pad;
+};
+
+template <int G>
+struct Qk5Shape {
   static constexpr int WARPS = 4;
-  static constexpr int LIST = (sizeof(QkWarp<G>) + 127) & ~127;
-  static constexpr int PER_WARP = LIST + NB * Q3_SLOT;
+  static constexpr int NB = 5;  // ring slots per warp
+  static constexpr int LIST = (sizeof(Qk5Warp<G>) + 127) & ~127;
+  static constexpr int PER_WARP = LIST + NB * Q5_SLOT;
   static constexpr int SMEM = WARPS * PER_WARP;
-  static constexpr int MINB = G == 1 ? 3 : 2;
+  static constexpr int MINB = 2;
+  static_assert(G * Q5_CHUNKS * 8 * 3 <= NB * Q5_SLOT, "prologue scratch must fit the ring");
 };
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -461,63 +511,285 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int G>
-__device__ __forceinline__ void q3_issue(uint8_t* slot, const QkWarp<G>& ws, int b, bool full, const uint8_t* base) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
-  const uint4 o = *reinterpret_cast<const uint4*>(&ws.off[8 * b + 4 * half]);
-  const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+// Rule 1 + lists, B fragments and variant masks.  Runs with the ring drained
+// (its memory holds the per-position q / code scratch).
+template <int G, bool TRUNC>
+__device__ void k5_prologue(Qk5Warp<G>& ws, uint8_t* scratch, const akv_store_t& s, const akv_cfg_t& cfg,
+                            const akv_step_t& st, int u, int n, bool book) {
+  const int lane = threadIdx.x & 31;
+  uint16_t(*qh)[Q5_CHUNKS * 8] = reinterpret_cast<uint16_t(*)[Q5_CHUNKS * 8]>(scratch);
+  uint8_t(*cd)[Q5_CHUNKS * 8] = reinterpret_cast<uint8_t(*)[Q5_CHUNKS * 8]>(scratch + G * Q5_CHUNKS * 8 * 2);
+  uint32_t qw[G][4];
+  int code[G][4], ucode[4];
+  k_rule1<G, TRUNC>(s, cfg, st, u, n, book, qw, code, ucode);
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t b8[4], bf[4];
+  int n8 = 0, nf = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) cp_async16(slot + (2 * i + half) * 256 + l16 * 16, base + ov[i] + l16 * 16);
-  if (full) {
+  for (int k = 0; k < 4; ++k) {
+    b8[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] == 8);
+    bf[k] = __ballot_sync(0xFFFFFFFFu, ucode[k] >= 12);
+    n8 += __popc(b8[k]);
+    nf += __popc(bf[k]);
+  }
+  // at least one slot per page, so an all-SKIP unit still writes its (zero) scores
+  const int n8p = (n8 + nf == 0) ? 16 : (n8 + 15) & ~15, nlp = n8p + ((nf + 7) & ~7);
+  // pads: channel 0's rows, q = 0, code 0
+  for (int pos = lane; pos < Q5_CHUNKS * 8; pos += 32) {
+    ws.off[pos] = 0u;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      qh[j][pos] = 0;
+      cd[j][pos] = 0;
+    }
+  }
+  if (lane < (Q5_CHUNKS * 8 + 31) / 32) ws.low[lane] = 0u;
+  __syncwarp();
+  int base8 = 0, basef = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = lane + 32 * k;
+    int pos = -1;
+    if (ucode[k] == 8) pos = base8 + __popc(b8[k] & lt);
+    else if (ucode[k] >= 12) pos = n8p + basef + __popc(bf[k] & lt);
+    if (pos >= 0) {
+      ws.off[pos] = (uint32_t)c * P;
+      if (ucode[k] == 16) atomicOr(&ws.low[pos >> 5], 1u << (pos & 31));
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        qh[j][pos] = code[j][k] ? (uint16_t)(qw[j][k] & 0xFFFFu) : (uint16_t)0;
+        cd[j][pos] = (uint8_t)code[j][k];
+      }
+    }
+    base8 += __popc(b8[k]);
+    basef += __popc(bf[k]);
+  }
+  __syncwarp();
+  // B fragments: lane (g, t) holds head g's q at list positions 2t, 2t+1 of the chunk
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = nlp >> 3, n8c = n8p >> 3;
+  for (int c = 0; c < nch; ++c) {
+    const int p0 = c * 8 + 2 * t;
+    uint32_t q0 = 0u, q1 = 0u, c0 = 0u, c1 = 0u;
+    if (g < G) {
+      q0 = qh[g][p0];
+      q1 = qh[g][p0 + 1];
+      c0 = cd[g][p0];
+      c1 = cd[g][p0 + 1];
+    }
+    uint32_t vm = 0u;
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+      const uint32_t tier = 8u + 4u * v;
+      const uint32_t b = (c0 == tier ? q0 : 0u) | ((c1 == tier ? q1 : 0u) << 16);
+      ws.bf[c][v][lane] = b;
+      if (__any_sync(0xFFFFFFFFu, b != 0u)) vm |= 1u << v;
+    }
+    if (lane == 0) ws.vmask[c] = (uint8_t)(c < n8c ? 1u : vm);
+  }
+  if (lane == 0) {
+    ws.n8p = n8p;
+    ws.nlp = nlp;
+    ws.unit = u;
+  }
+  __syncwarp();
+}
+
+// Copy slot b of a page into the ring (one commit group).
+template <int G>
+__device__ __forceinline__ void q5_issue(uint8_t* slot, const Qk5Warp<G>& ws, int b, const uint8_t* base) {
+  const int lane = threadIdx.x & 31;
+  const int n8s = ws.n8p >> 4;
+  if (b < n8s) {
+    const int p0 = 16 * b;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = lane + 32 * k, r = idx >> 4, col = idx & 15;
+      cp_async16(slot + r * 256 + col * 16, base + ws.off[p0 + r] + col * 16);
+    }
+  } else {
+    const int p0 = ws.n8p + 8 * (b - n8s);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = lane + 32 * k, r = idx >> 4, col = idx & 15;
+      cp_async16(slot + r * 256 + col * 16, base + ws.off[p0 + r] + col * 16);
+    }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const int idx = lane * 2 + k, pib = idx >> 3, chunk = idx & 7;
-      const int sl = 8 * b + 4 * (pib & 1) + (pib >> 1);
-      const uint32_t off = ws.off[sl] >> 1;
-      cp_async16(slot + 2048 + pib * 128 + chunk * 16, base + MID + off + chunk * 16);
-      if ((ws.low[sl >> 5] >> (sl & 31)) & 1u) cp_async16(slot + 3072 + pib * 128 + chunk * 16, base + LOW + off + chunk * 16);
+      const int idx = lane + 32 * k, r = idx >> 3, col = idx & 7;
+      const int pos = p0 + r;
+      const uint8_t* src = base + MID + (ws.off[pos] >> 1) + col * 16;
+      uint8_t* dst = slot + 2048 + r * 128 + ((col ^ (((r >> 1) & 1) << 2)) << 4);
+      cp_async16(dst, src);
+      if ((ws.low[pos >> 5] >> (pos & 31)) & 1u) cp_async16(dst + 1024, src + (LOW - MID));
     }
   }
   cp_async_commit();
 }
 
-template <int HG, bool FULL, bool TRUNC, int G>
-__device__ __forceinline__ void q3_compute(const uint8_t* slot, const QkWarp<G>& ws, int b, int j0,
-                                           float (&acc)[HG][16], uint32_t tkm, uint32_t tf) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
-  KBatch X;
-  const uint32_t lowm = FULL ? (ws.low[(8 * b) >> 5] >> ((8 * b + 4 * half) & 31)) & 0xFu : 0u;
+struct K5Head {
+  uint4 h[2][2];  // [channel][page half]: 16 tokens each
+};
+struct K5Nib {
+  uint2 m[2][2], l[2][2];
+};
+
+__device__ __forceinline__ uint32_t u4w(const uint4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ void mma_f16_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b));
+}
+
+// (x & m) | f as one LOP3 with both constants in registers
+__device__ __forceinline__ uint32_t mask_fill(uint32_t x, uint32_t m, uint32_t f) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "r"(m), "r"(f));
+  return r;
+}
+
+__device__ __forceinline__ void k5_compute_t8(const K5Head& X, uint32_t b8, float (&acc)[16][4], uint32_t c80) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int pib = 2 * i + half;
-    X.h[i] = *reinterpret_cast<const uint4*>(slot + pib * 256 + l16 * 16);
-    if (FULL) {
-      X.m[i] = *reinterpret_cast<const uint2*>(slot + 2048 + pib * 128 + l16 * 8);
-      X.l[i] = ((lowm >> i) & 1u) ? *reinterpret_cast<const uint2*>(slot + 3072 + pib * 128 + l16 * 8)
-                                  : make_uint2(0x88888888u, 0x88888888u);
-    } else if (G > 1) {
-      X.m[i] = make_uint2(0x88888888u, 0x88888888u);
-      X.l[i] = make_uint2(0u, 0u);
+  for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // token 16g + 2i (of the half) is byte 2i of the lane's 16 head bytes of each channel
+      const int wi = i >> 1, p = 2 * (i & 1);
+      // x = (ch0 token 2i, ch0 token 2i+1, ch1 token 2i, ch1 token 2i+1), then the head
+      // bytes into positions 1 and 3 with the 0x80 midpoint fill in 0 and 2
+      const uint32_t x = prmt(u4w(X.h[0][hf], wi), u4w(X.h[1][hf], wi), (uint32_t)(((5 + p) << 12) | ((4 + p) << 8) |
+                                                                                       ((p + 1) << 4) | p));
+      mma_f16_1688(acc[8 * hf + i], prmt(x, c80, 0x2404), prmt(x, c80, 0x3414), b8);
     }
-  }
-  k_compute<HG, (FULL || G > 1), TRUNC, G>(X, ws, b, half, j0, acc, tkm, tf);
+}
+
+// vmr: the tier variants present in the chunk (bit 0 T8, 1 T12, 2 T16; VM == 8 reads
+// vmr at run time).  Specialising every combination (VM 1..7) is slower: the code
+// growth costs more than the predicated-off mma (measured, profiles/r01_history.md).
+template <bool TRUNC, int VM>
+__device__ __forceinline__ void k5_compute_full(const K5Head& X, const K5Nib& N, uint32_t b8, uint32_t b12,
+                                                uint32_t b16, float (&acc)[16][4], uint32_t tkm, uint32_t tf,
+                                                uint32_t c80, uint32_t vmr = 0) {
+  uint32_t m12 = 0xFFF0FFF0u, f12 = 0x00080008u;
+  asm volatile("" : "+r"(m12), "+r"(f12));  // keep the T12 mask / fill in registers (one LOP3 per word)
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+    for (int hv = 0; hv < 2; ++hv) {  // tokens 8hv .. 8hv+7 of the lane's 16 in this half
+      uint32_t W[2][4];  // per channel: token pairs (2k, 2k+1) at the union tier
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        assemble8(hv ? X.h[j][hf].z : X.h[j][hf].x, hv ? X.h[j][hf].w : X.h[j][hf].y,
+                  hv ? N.m[j][hf].y : N.m[j][hf].x, hv ? N.l[j][hf].y : N.l[j][hf].x, W[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = 8 * hf + 4 * hv + k;
+        uint32_t a0 = prmt(W[0][k], W[1][k], 0x5410), a1 = prmt(W[0][k], W[1][k], 0x7632);
+        if (TRUNC) {
+          a0 = mask_fill(a0, tkm, tf);
+          a1 = mask_fill(a1, tkm, tf);
+        }
+        const uint32_t vm = VM == 8 ? vmr : (uint32_t)VM;
+        if (vm & 4u) mma_f16_1688(acc[i], a0, a1, b16);
+        if (vm & 2u) mma_f16_1688(acc[i], mask_fill(a0, m12, f12), mask_fill(a1, m12, f12), b12);
+        if (vm & 1u) mma_f16_1688(acc[i], prmt(a0, c80, 0x3414), prmt(a1, c80, 0x3414), b8);
+      }
+    }
 }
 
 template <int G, bool TRUNC>
-__global__ void __launch_bounds__(32 * Qk3Shape<G>::WARPS, Qk3Shape<G>::MINB)
-    qk3_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, float isd, int npg_max) {
-  using S = Qk3Shape<G>;
-  constexpr int HG = S::HG, NB = S::NB, NPASS = G / HG;
+__device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>& ws, int b, float (&acc)[16][4],
+                                           uint32_t tkm, uint32_t tf, uint32_t c80) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int n8s = ws.n8p >> 4;
+  if (b < n8s) {
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      K5Head X;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+          X.h[j][hf] = *reinterpret_cast<const uint4*>(slot + (8 * cc + 2 * t + j) * 256 + 128 * hf + 16 * g);
+      k5_compute_t8(X, ws.bf[2 * b + cc][0][lane], acc, c80);
+    }
+  } else {
+    const int ch = (ws.n8p >> 3) + (b - n8s), p0 = ws.n8p + 8 * (b - n8s) + 2 * t;
+    const uint32_t lowm = (ws.low[p0 >> 5] >> (p0 & 31)) & 3u;
+    K5Head X;
+    K5Nib N;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = 2 * t + j;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        X.h[j][hf] = *reinterpret_cast<const uint4*>(slot + r * 256 + 128 * hf + 16 * g);
+        const int nb = 2048 + r * 128 + ((64 * hf + 8 * g) ^ ((t & 1) << 6));
+        N.m[j][hf] = *reinterpret_cast<const uint2*>(slot + nb);
+        N.l[j][hf] = ((lowm >> j) & 1u) ? *reinterpret_cast<const uint2*>(slot + nb + 1024)
+                                        : make_uint2(0x88888888u, 0x88888888u);
+      }
+    }
+    const uint32_t b8 = ws.bf[ch][0][lane], b12 = ws.bf[ch][1][lane], b16 = ws.bf[ch][2][lane];
+    const uint32_t vm = ws.vmask[ch];
+    k5_compute_full<TRUNC, 8>(X, N, b8, b12, b16, acc, tkm, tf, c80, vm);
+  }
+}
+
+// Scale, store and summarise one head's 16 tokens (16g .. 16g+15 of a page half);
+// a 32-token chunk = lanes g = 2c, 2c+1 (lane ^ 4).
+__device__ __forceinline__ void k5_finish(const float (&raw)[16], int tok0, int n, float* scores_h, float* stats_h,
+                                          float isd, bool store) {
+  const int lane = threadIdx.x & 31;
+  const int nv = min(max(n - tok0, 0), 16);
+  float sv[16];
+  float m = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    sv[e] = raw[e] * isd;
+    if (e < nv) m = fmaxf(m, sv[e]);
+  }
+  m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 4));
+  float l = 0.f;
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if (e < nv) l += expf(sv[e] - m);
+  l += __shfl_xor_sync(0xFFFFFFFFu, l, 4);
+  if (!store) return;  // (lanes of absent heads: the shuffles above need the whole warp)
+  float* out = scores_h + tok0;
+  if (nv == 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      reinterpret_cast<float4*>(out)[q] = make_float4(sv[4 * q], sv[4 * q + 1], sv[4 * q + 2], sv[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (e < nv) out[e] = sv[e];
+  }
+  if (((lane >> 2) & 1) == 0 && tok0 < n) {  // even g owns the chunk
+    float* ps = stats_h + (tok0 >> 5) * 2;
+    ps[0] = m;
+    ps[1] = l;
+  }
+}
+
+template <int G, bool TRUNC>
+__global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
+    qk5_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, float isd, int npg_max) {
+  using S = Qk5Shape<G>;
+  constexpr int NB = S::NB;
   pdl_trigger();
   pdl_wait();
-  extern __shared__ __align__(128) uint8_t qk3_smem[];
+  extern __shared__ __align__(128) uint8_t qk5_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = lane >> 4, l16 = lane & 15;
-  QkWarp<G>& ws = *reinterpret_cast<QkWarp<G>*>(qk3_smem + warp * S::PER_WARP);
-  uint8_t* ring = qk3_smem + warp * S::PER_WARP + S::LIST;
-  if (lane == 0) ws.unit = -1;
-  __syncwarp();
-  uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
+  const int g = lane >> 2, t = lane & 3;
+  Qk5Warp<G>& ws = *reinterpret_cast<Qk5Warp<G>*>(qk5_smem + warp * S::PER_WARP);
+  uint8_t* ring = qk5_smem + warp * S::PER_WARP + S::LIST;
+  uint32_t tkm = 0xFFFFFFFFu, tf = 0u, c80 = 0x80808080u;
+  asm volatile("" : "+r"(c80));
   if (TRUNC) {
     const int kb = cfg.trunc_bits - 6;
     const uint32_t km = (0xFFFFu << (10 - kb)) & 0xFFFFu;
@@ -525,139 +797,128 @@ __global__ void __launch_bounds__(32 * Qk3Shape<G>::WARPS, Qk3Shape<G>::MINB)
     tkm = km | (km << 16);
     tf = fill | (fill << 16);
   }
-  // balanced contiguous range of (unit, page, head-pass) items
-  const long long total = (long long)s.n_units * npg_max * NPASS;
+  // balanced contiguous range of (unit, page) items
+  const long long total = (long long)s.n_units * npg_max;
   const long long nw = (long long)gridDim.x * S::WARPS, gw = (long long)blockIdx.x * S::WARPS + warp;
   const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
   const int cap_chunks = s.max_pages * (P / 32);
 
-  // load cursor (li, lb) and compute cursor (ci, cb) over (item, batch); both walk the same items
+  // load cursor (li, lb) and compute cursor (ci, cb) over (item, slot); both walk the same items
   UnitPages lup, cup;
   lup.u = cup.u = -1;
   lup.n = cup.n = 0;
-  long long li = i0, ci = i0;
-  int lb = 0, cb = 0;
-  const uint8_t* lbase = nullptr;
-  bool lblocked = false;  // the load cursor reached a unit whose Rule-1 lists are not built yet
-  int issued = 0, computed = 0;
-  float acc[HG][16];
-#pragma unroll
-  for (int jj = 0; jj < HG; ++jj)
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[jj][e] = 0.f;
-
-  // next valid item at or after i (page inside its unit's length)
   auto seek = [&](long long i, UnitPages& up) -> long long {
     for (; i < i1; ++i) {
-      const long long pi = i / NPASS;
-      const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
+      const int u = (int)(i / npg_max), pg = (int)(i % npg_max);
       if (u != up.u) unit_pages_fetch(up, s, u);
       if (pg * P < up.n) return i;
     }
     return i1;
   };
-  li = seek(li, lup);
-  ci = li;
+  long long li = seek(i0, lup), ci = li;
   cup = lup;
+  int lb = 0, cb = 0, issued = 0, computed = 0;
+  bool lblocked = false;  // the load cursor reached a unit whose lists are not built yet
+  const uint8_t* lbase = nullptr;
   if (li < i1) {
-    const long long pi = li / NPASS;
-    k_prologue<G, TRUNC>(ws, s, cfg, st, (int)(pi / npg_max), lup.n, pi % npg_max == 0);
-    lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+    const int pg = (int)(li % npg_max);
+    k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, (int)(li / npg_max), lup.n, pg == 0);
+    lbase = s.k_pool + unit_page(lup, s, pg) * PAGE;
   }
+  float acc[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
   while (ci < i1) {
-    // issue up to NB-1 batches ahead (stop at a unit whose lists are not built)
+    const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
+    // issue up to NB-1 slots ahead (stop at a unit whose lists are not built)
     while (li < i1 && !lblocked && issued - computed < NB - 1) {
-      const int nb8 = ws.n8p >> 3;
-      q3_issue<G>(ring + (issued % NB) * Q3_SLOT, ws, lb, lb >= nb8, lbase);
+      q5_issue<G>(ring + (issued % NB) * Q5_SLOT, ws, lb, lbase);
       ++issued;
-      if (++lb == (ws.nlist >> 3)) {
+      if (++lb == nslots) {
         lb = 0;
-        const long long pu = li / NPASS / npg_max;
+        const long long pu = li / npg_max;
         li = seek(li + 1, lup);
         if (li < i1) {
-          const long long pi = li / NPASS;
-          if (pi / npg_max != pu) lblocked = true;  // new unit: wait for the math to drain
-          else lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+          if (li / npg_max != pu) lblocked = true;  // new unit: wait for the math to drain
+          else lbase = s.k_pool + unit_page(lup, s, (int)(li % npg_max)) * PAGE;
         }
       }
     }
     if (issued == computed) {
       // drained at a unit boundary: build the next unit's lists, resume loading
-      const long long pi = li / NPASS;
-      k_prologue<G, TRUNC>(ws, s, cfg, st, (int)(pi / npg_max), lup.n, pi % npg_max == 0);
-      lbase = s.k_pool + unit_page(lup, s, (int)(pi % npg_max)) * PAGE;
+      const int pg = (int)(li % npg_max);
+      k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, (int)(li / npg_max), lup.n, pg == 0);
+      lbase = s.k_pool + unit_page(lup, s, pg) * PAGE;
       lblocked = false;
       continue;
     }
     const int inflight = issued - computed;  // 1 .. NB-1
-    if (inflight >= 3) cp_async_wait<2>();
+    if (inflight >= 4) cp_async_wait<3>();
+    else if (inflight == 3) cp_async_wait<2>();
     else if (inflight == 2) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncwarp();
-    const int nb8 = ws.n8p >> 3;
-    const long long pi = ci / NPASS;
-    const int j0 = (int)(ci % NPASS) * HG;
-    const uint8_t* slot = ring + (computed % NB) * Q3_SLOT;
-    if (G > 1 || cb >= nb8) q3_compute<HG, true, TRUNC, G>(slot, ws, cb, j0, acc, tkm, tf);
-    else q3_compute<HG, false, TRUNC, G>(slot, ws, cb, j0, acc, tkm, tf);
+    q5_compute<G, TRUNC>(ring + (computed % NB) * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
     ++computed;
     __syncwarp();  // every lane is done with the slot before it is refilled
-    if (++cb == (ws.nlist >> 3)) {
-      // page done: fold the half-warps, scale, store, chunk stats
-      const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
+    if (++cb == nslots) {
+      // page done: lane (g, t) holds tokens 16g + 2i (acc[i][0..1]) and 16g + 2i + 1
+      // (acc[i][2..3]) of each page half for heads 2t, 2t+1
+      const int u = (int)(ci / npg_max), pg = (int)(ci % npg_max);
       if (u != cup.u) unit_pages_fetch(cup, s, u);
       const int n = cup.n;
 #pragma unroll
-      for (int jj = 0; jj < HG; ++jj) {
-        float mine[8];
+      for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float lo = acc[jj][e] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e], 16);
-          const float hi = acc[jj][e + 8] + __shfl_xor_sync(0xFFFFFFFFu, acc[jj][e + 8], 16);
-          mine[e] = half ? hi : lo;
+        for (int hh = 0; hh < 2; ++hh) {
+          float raw[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            raw[2 * i] = acc[8 * hf + i][hh];
+            raw[2 * i + 1] = acc[8 * hf + i][2 + hh];
+          }
+          const int j = 2 * t + hh;
+          const size_t h = (size_t)u * G + (j < G ? j : 0);
+          k5_finish(raw, pg * P + 128 * hf + 16 * g, n, st.scores + h * cap, st.page_stats + h * cap_chunks * 2,
+                    isd, j < G);
         }
-        const size_t hh = (size_t)u * G + j0 + jj;
-        qk_finish(mine, pg * P + 16 * l16 + 8 * half, n, st.scores + hh * cap, st.page_stats + hh * cap_chunks * 2,
-                  isd);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) acc[jj][e] = 0.f;
-      }
+      for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       cb = 0;
       ci = seek(ci + 1, cup);
     }
   }
 }
 
-// The cp.async-ring variant wins for GQA groups (G >= 4: the register pipeline
-// cannot hold enough batches next to 4 heads' accumulators); for G <= 2 the
-// register pipeline is faster (measured, profiles/r01_history.md).
-
 template <int G, bool TRUNC>
-static void launch_qk3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
+static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
-  using S = Qk3Shape<G>;
+  using S = Qk5Shape<G>;
   static int resident = 0;
   if (!resident) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(qk3_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk3_kernel<G, TRUNC>, 32 * S::WARPS, S::SMEM);
+    cudaFuncSetAttribute(qk5_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk5_kernel<G, TRUNC>, 32 * S::WARPS, S::SMEM);
     resident = sms * std::max(per, 1);
   }
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
-  const long long items = (long long)s.n_units * npg * (G / S::HG);
+  const long long items = (long long)s.n_units * npg;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
   const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  launch_pdl(qk3_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
+  launch_pdl(qk5_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
 }
 
+// G <= 2: the direct-load FHFMA kernel; G >= 4: the tensor-core ring kernel (one
+// K tile feeds 4-8 heads, so the FHFMA path would be issue bound).
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
-  if (G >= 4) {
-    launch_qk3_t<G, TRUNC>(s, cfg, st, max_len, stream);
+  if constexpr (G >= 4) {
+    launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
     return;
   }
   static int resident = 0;

@@ -124,18 +124,22 @@ def test_gqa_parity(g):
     _compare_case(Case(B=1, Hkv=2, g=g, n=513, seed=40 + g))
 
 
-def test_flat_scales_parity():
-    """Paper-like regime (U[-0.5,0.5]): many T12/T16 reads and element-path V rows."""
-    c = Case(B=2, Hkv=2, g=2, n=700, seed=5, lo=-0.5, hi=0.5)
+@pytest.mark.parametrize("g", [2, 8])
+def test_flat_scales_parity(g):
+    """Paper-like regime (U[-0.5,0.5]): many T12/T16 reads and element-path V rows
+    (g = 8: chunks mixing all three K tier variants in the tensor-core qk)."""
+    c = Case(B=2, Hkv=2, g=g, n=700, seed=5, lo=-0.5, hi=0.5)
     r = _compare_case(c)
     st = r.v_stats()
     assert st.t12 + st.t16 > st.elements_read * 0.001
 
 
-@pytest.mark.parametrize("margin,zero_skip", [(-2, True), (4, True), (0, False)])
-def test_config_parity(margin, zero_skip):
-    c = Case(B=1, Hkv=2, g=2, n=300, seed=77)
+@pytest.mark.parametrize("margin,zero_skip,g", [(-2, True, 2), (4, True, 2), (0, False, 2), (0, True, 4),
+                                               (3, False, 4)])
+def test_config_parity(margin, zero_skip, g):
+    c = Case(B=1, Hkv=2, g=g, n=300, seed=77)
     c.Q[0, 0, :5] = 0  # zero q channels exercise D1
+    c.Q[1, :, 40:48] = 0  # ... in every head of a unit: SKIP for the whole group under zero_skip
     c.q = torch.from_numpy(c.Q.view(np.int16)).view(c.B, c.Hkv * c.g, 128)
     _compare_case(c, AlignConfig(margin, zero_skip), OAlignConfig(margin, zero_skip))
 
@@ -144,9 +148,9 @@ def test_row_strategy_parity():
     _compare_case(Case(B=1, Hkv=2, g=2, n=400, seed=9, lo=-1, hi=1), strategy="row")
 
 
-@pytest.mark.parametrize("tier", [8, 12, 16])
-def test_forced_tier_parity(tier):
-    _compare_case(Case(B=1, Hkv=2, g=1, n=300, seed=3), force=tier)
+@pytest.mark.parametrize("tier,g", [(8, 1), (12, 1), (16, 1), (8, 4), (12, 4), (16, 8)])
+def test_forced_tier_parity(tier, g):
+    _compare_case(Case(B=1, Hkv=2, g=g, n=300, seed=3), force=tier)
 
 
 def test_forced_t16_equals_reference_paths():
@@ -167,8 +171,9 @@ def test_forced_t16_equals_reference_paths():
     assert close(r.o.view(4, 2, 128).cpu().numpy(), o_t.cpu().numpy())
 
 
-def test_baseline_truncated_parity():
-    c = Case(B=1, Hkv=2, g=1, n=300, seed=8)
+@pytest.mark.parametrize("g", [1, 4])
+def test_baseline_truncated_parity(g):
+    c = Case(B=1, Hkv=2, g=g, n=300, seed=8)
     r = c.gpu()
     s_b, o_b = AD.baseline_truncated(c.q, c.store, r.probs, 13)
     for u, b, hq, j in c.units():

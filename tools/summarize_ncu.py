@@ -73,10 +73,15 @@ def launches(path: str) -> str:
 
 
 def full(path: str) -> str:
-    res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
-    if res.returncode != 0:
-        return "ncu -i failed:\n" + res.stderr
-    rd = list(csv.reader(io.StringIO(res.stdout)))
+    if path.endswith(".csv"):  # an exported `--page raw --csv`
+        with open(path) as f:
+            text = f.read()
+    else:
+        res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
+        if res.returncode != 0:
+            return "ncu -i failed:\n" + res.stderr
+        text = res.stdout
+    rd = list(csv.reader(io.StringIO(text)))
     hdr, units = rd[0], rd[1]
     idx = {h: i for i, h in enumerate(hdr)}
     out = []
