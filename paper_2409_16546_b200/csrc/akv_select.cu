@@ -35,7 +35,15 @@ struct SelSmem {
   int wfirst[SW];
   int sel_page[AKV_MAX_KSEL];
   int tmin[4], tunk[4];
+  // ST = 256 (max_len <= 8192): the per-token fetch-plan bound of step 6, computed in
+  // step 2 next to p (no reload of p / RowMax), and the selection bitmap
+  int16_t xs[ST == 256 ? 8192 : 1];
+  uint32_t selw[ST == 256 ? 8192 / 32 : 1];
 };
+
+// xs sentinels: p = 0 (never fetched unless the row strategy has unknown targets),
+// row strategy with RowMax = 0 (T8)
+constexpr int16_t XS_P0 = -32768, XS_RM0 = -32767;
 
 __device__ __forceinline__ uint32_t v_word_exact(const uint8_t* vp, int tt, int r) {
   const uint32_t head = vp[tt * D + r];
@@ -63,11 +71,15 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 1) select_kernel(akv_store
   // the first batch of scores is loaded before the statistics are known (overlaps step 1)
   constexpr int BT = 8;
   const float* sc = st.scores + (size_t)h * cap;
+  constexpr bool FASTNEED = ST == 256;
+  const uint16_t* rmu = s.rowmax + (size_t)u * s.max_pages * P;
   float sv0[BT];
+  uint32_t rm0[BT];
 #pragma unroll
   for (int b = 0; b < BT; ++b) {
     const int t = b * ST + tid;
     sv0[b] = t < n ? sc[t] : 0.f;
+    rm0[b] = FASTNEED && t < n ? (uint32_t)rmu[t] : 0u;
   }
 
   // 1. global softmax statistics (fixed assignment + butterfly: deterministic); the
@@ -102,37 +114,67 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 1) select_kernel(akv_store
   }
   __syncthreads();
   const float M = sm.M, L = sm.L;
-  const float pmax = 1.0f / L;  // = expf(0) / L, the argmax token's p
-  const float thr = ldexpf(pmax, -cfg.m);
   const float invL = 1.0f / L;
+  const float pmax = invL;  // = expf(0) / L, the argmax token's p
+  const float thr = ldexpf(pmax, -cfg.m);
   const bool est = cfg.force_tier == 0 && cfg.trunc_bits == 0 && cfg.k_sel > 0;  // k_sel = 0: softmax only
   const int k_sel = max(min(cfg.k_sel, AKV_MAX_KSEL), 1);
   float* pr = st.probs + (size_t)h * cap;
   uint32_t* bits = st.sel_bits + (size_t)h * (cap >> 5);
 
-  // 2. probabilities, bitmap reset, candidate compaction (loads batched BT deep)
+  // 2. probabilities, bitmap reset, candidate compaction: batches of BT tokens per thread,
+  //    the next batch's scores (and RowMax words) loaded before the current one is used.
+  //    p = exp(s - M) * (1/L): one rounding more than a division (~1 ulp, far inside the
+  //    2^-18 knife-edge margin of D11) and no division slow path.
+  for (int w = tid; w < (n + 31) / 32; w += ST) {
+    bits[w] = 0u;
+    if (FASTNEED) sm.selw[w] = 0u;
+  }
+  const float* scb = sc + tid;
+  const uint16_t* rmb = rmu + tid;
+  float* prb = pr + tid;
   for (int t0 = 0; t0 < n; t0 += ST * BT) {
     float sv[BT];
+    uint32_t rmv[BT];
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
-      const int t = t0 + b * ST + tid;
-      sv[b] = t0 == 0 ? sv0[b] : (t < n ? sc[t] : 0.f);
+      sv[b] = sv0[b];
+      rmv[b] = rm0[b];
+    }
+    const int t1 = t0 + ST * BT;
+    if (t1 < n) {
+      if (t1 + ST * BT <= n) {
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+          sv0[b] = scb[t1 + b * ST];
+          rm0[b] = FASTNEED ? (uint32_t)rmb[t1 + b * ST] : 0u;
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+          const bool in = t1 + b * ST + tid < n;
+          sv0[b] = in ? scb[t1 + b * ST] : 0.f;
+          rm0[b] = FASTNEED && in ? (uint32_t)rmb[t1 + b * ST] : 0u;
+        }
+      }
     }
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
       const int t = t0 + b * ST + tid;
-      bool cand = false;
-      float p = 0.f;
-      if (t < n) {
-        // exact IEEE division where p can matter; for exp(d) < e^-69 (~1e-30, far below every
-        // threshold, tier boundary and the 1e-3 output tolerance) multiply by 1/L instead, which
-        // keeps the division's denormal slow path out of the common near-one-hot case
-        const float dlt = sv[b] - M;
-        p = dlt > -69.f ? expf(dlt) / L : expf(dlt) * invL;
-        pr[t] = p;
-        cand = est && p >= thr;
+      const bool in = t < n;
+      const float p = expf(sv[b] - M) * invL;
+      const bool cand = in && est && p >= thr;
+      if (in) {
+        prb[t0 + b * ST] = p;
+        if (FASTNEED) {
+          const uint32_t rm = rmv[b];
+          int x;
+          if (p == 0.f) x = XS_P0;
+          else if (cfg.strategy == 1) x = rm == 0 ? XS_RM0 : floor_log2f(p) + magexp16(rm) + cfg.margin_bits;
+          else x = floor_log2f(p) + max(bexp16(rm), 1) - 15 + cfg.margin_bits;
+          sm.xs[t] = (int16_t)x;
+        }
       }
-      if (lane == 0 && t < n) bits[t >> 5] = 0u;
       const unsigned bb = __ballot_sync(0xFFFFFFFFu, cand);
       if (bb) {
         int base = 0;
@@ -266,6 +308,7 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 1) select_kernel(akv_store
     sm.sel_sorted[rank] = t;
     sm.sel_page[rank] = s.page_table[(size_t)u * s.max_pages + t / P];
     atomicOr(bits + (t >> 5), 1u << (t & 31));
+    if (FASTNEED) atomicOr(&sm.selw[t >> 5], 1u << (t & 31));
   }
   __syncthreads();
   // rows split over warps (warp w: rows w, w+8, ...), lane = 4 channels; fixed-order reduction.
@@ -326,7 +369,33 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 1) select_kernel(akv_store
   const int unk_all = sm.tunk[0] + sm.tunk[1] + sm.tunk[2] + sm.tunk[3];
   // 6. V rows needing the mid / low nibble row for this head (PV fetch plan):
   //    element strategy: RowMax superset bound (H6); row strategy: the row tier (D7)
-  {
+  if (FASTNEED) {
+    // from the bounds of step 2: bound - tmin > 2 (mid) / > 6 (low), i.e. the row tier >= 12 / 16
+    uint32_t* nb = st.need_bits + (size_t)h * 2 * (cap >> 5);
+    for (int w = warp; w < (n + 31) / 32; w += ST / 32) {
+      const int t = 32 * w + lane;
+      bool nm = false, nlw = false;
+      if (t < n && est) {
+        const int x = sm.xs[t];
+        if (cfg.strategy == 1) {
+          if (unk_all) nm = nlw = true;
+          else if (x != XS_P0 && x != XS_RM0) {
+            nm = x - tmin_all > 2;
+            nlw = x - tmin_all > 6;
+          }
+        } else if (x != XS_P0) {
+          nm = unk_all || x - tmin_all > 2;
+          nlw = unk_all || x - tmin_all > 6;
+        }
+      }
+      const uint32_t sw = sm.selw[w];
+      const unsigned bm = __ballot_sync(0xFFFFFFFFu, nm) & ~sw, bl = __ballot_sync(0xFFFFFFFFu, nlw) & ~sw;
+      if (lane == 0) {
+        nb[w] = bm;
+        nb[(cap >> 5) + w] = bl;
+      }
+    }
+  } else {
     uint32_t* nb = st.need_bits + (size_t)h * 2 * (cap >> 5);
     for (int t0 = 0; t0 < n; t0 += ST * BT) {
       float pv[BT];
