@@ -1,0 +1,17 @@
+"""Small decode steps for compute-sanitizer beyond smoke(): GQA groups (qk5 tensor-core
+kernel, pv quad path), forced tiers and truncation.  Exits non-zero on a parity failure."""
+import os
+import sys
+
+ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+from gpu_helpers import Case, close  # noqa: E402
+
+for g, n, kw in [(4, 600, {}), (8, 300, {}), (4, 300, {"force_tier": 12})]:
+    c = Case(B=1, Hkv=2, g=g, n=n, seed=5)
+    r = c.gpu(**kw)
+    o = r.o.cpu().numpy()
+    for u, b, hq, j in c.units():
+        ref = c.oracle(u, j, force_tier=kw.get("force_tier"))
+        assert close(o[b, hq], ref.o), (g, n, kw, u, j)
+    print(f"g={g} n={n} {kw} ok")
