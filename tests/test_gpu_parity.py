@@ -335,3 +335,9 @@ def test_decode_graph_copy_modes(zin, zout):
 def test_long_context_beyond_register_page_table():
     """n = 33000 tokens = 129 pages: pages >= 128 take the page-table fallback path."""
     _compare_case(Case(B=1, Hkv=1, g=1, n=33000, seed=123))
+
+
+def test_gqa_long_context():
+    """g = 8 over 40 pages (n > 8192: the 1024-thread select; qk5 rings continuous across
+    many pages of a unit; pv quad path)."""
+    _compare_case(Case(B=1, Hkv=1, g=8, n=10000, seed=17))
