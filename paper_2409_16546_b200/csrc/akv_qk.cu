@@ -666,15 +666,15 @@ __device__ __forceinline__ void k5_compute_t8(const K5Head& X, uint32_t b8, floa
     }
 }
 
-// vmr: the tier variants present in the chunk (bit 0 T8, 1 T12, 2 T16; VM == 8 reads
-// vmr at run time).  Specialising every combination (VM 1..7) is slower: the code
-// growth costs more than the predicated-off mma (measured, profiles/r01_history.md).
-template <bool TRUNC, int VM>
-__device__ __forceinline__ void k5_compute_full(const K5Head& X, const K5Nib& N, uint32_t b8, uint32_t b12,
-                                                uint32_t b16, float (&acc)[16][4], uint32_t tkm, uint32_t tf,
-                                                uint32_t c80, uint32_t vmr = 0) {
-  uint32_t m12 = 0xFFF0FFF0u, f12 = 0x00080008u;
-  asm volatile("" : "+r"(m12), "+r"(f12));  // keep the T12 mask / fill in registers (one LOP3 per word)
+// vm: the tier variants present in the chunk (bit 0 T8, 1 T12, 2 T16).  The words are
+// rebuilt once at the union tier; each present variant is one warp-uniform branch over
+// the 16 tiles (no predicated-off mma; specialising every combination as a template
+// was slower: code growth, profiles/r01_history.md #32).
+template <bool TRUNC>
+__device__ __forceinline__ void k5_compute_full(const K5Head& X, const K5Nib& N, uint32_t vm, uint32_t b8,
+                                                uint32_t b12, uint32_t b16, float (&acc)[16][4], uint32_t tkm,
+                                                uint32_t tf, uint32_t c80) {
+  uint32_t A[16][2];
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
@@ -687,17 +687,29 @@ __device__ __forceinline__ void k5_compute_full(const K5Head& X, const K5Nib& N,
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int i = 8 * hf + 4 * hv + k;
-        uint32_t a0 = prmt(W[0][k], W[1][k], 0x5410), a1 = prmt(W[0][k], W[1][k], 0x7632);
+        A[i][0] = prmt(W[0][k], W[1][k], 0x5410);
+        A[i][1] = prmt(W[0][k], W[1][k], 0x7632);
         if (TRUNC) {
-          a0 = mask_fill(a0, tkm, tf);
-          a1 = mask_fill(a1, tkm, tf);
+          A[i][0] = mask_fill(A[i][0], tkm, tf);
+          A[i][1] = mask_fill(A[i][1], tkm, tf);
         }
-        const uint32_t vm = VM == 8 ? vmr : (uint32_t)VM;
-        if (vm & 4u) mma_f16_1688(acc[i], a0, a1, b16);
-        if (vm & 2u) mma_f16_1688(acc[i], mask_fill(a0, m12, f12), mask_fill(a1, m12, f12), b12);
-        if (vm & 1u) mma_f16_1688(acc[i], prmt(a0, c80, 0x3414), prmt(a1, c80, 0x3414), b8);
       }
     }
+  if (vm & 4u) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mma_f16_1688(acc[i], A[i][0], A[i][1], b16);
+  }
+  if (vm & 2u) {
+    uint32_t m12 = 0xFFF0FFF0u, f12 = 0x00080008u;
+    asm volatile("" : "+r"(m12), "+r"(f12));  // mask / fill in registers: one LOP3 per word
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      mma_f16_1688(acc[i], mask_fill(A[i][0], m12, f12), mask_fill(A[i][1], m12, f12), b12);
+  }
+  if (vm & 1u) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mma_f16_1688(acc[i], prmt(A[i][0], c80, 0x3414), prmt(A[i][1], c80, 0x3414), b8);
+  }
 }
 
 template <int G, bool TRUNC>
@@ -734,8 +746,7 @@ __device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>
       }
     }
     const uint32_t b8 = ws.bf[ch][0][lane], b12 = ws.bf[ch][1][lane], b16 = ws.bf[ch][2][lane];
-    const uint32_t vm = ws.vmask[ch];
-    k5_compute_full<TRUNC, 8>(X, N, b8, b12, b16, acc, tkm, tf, c80, vm);
+    k5_compute_full<TRUNC>(X, N, ws.vmask[ch], b8, b12, b16, acc, tkm, tf, c80);
   }
 }
 
