@@ -879,21 +879,47 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
       const int u = (int)(ci / npg_max), pg = (int)(ci % npg_max);
       if (u != cup.u) unit_pages_fetch(cup, s, u);
       const int n = cup.n;
+      if (G == 4) {
+        // heads 4..7 are padding: lanes t >= 2 take over page half 1 of lane t - 2, so
+        // every lane finishes 2 x 16 values instead of 4 x 16
+        const int hfe = t >> 1, src = t >= 2 ? lane - 2 : lane;
+        float mine[8][4];
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf)
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float v = __shfl_sync(0xFFFFFFFFu, acc[8 + i][e], src);
+            mine[i][e] = hfe ? v : acc[i][e];
+          }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           float raw[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            raw[2 * i] = acc[8 * hf + i][hh];
-            raw[2 * i + 1] = acc[8 * hf + i][2 + hh];
+            raw[2 * i] = mine[i][hh];
+            raw[2 * i + 1] = mine[i][2 + hh];
           }
-          const int j = 2 * t + hh;
-          const size_t h = (size_t)u * G + (j < G ? j : 0);
-          k5_finish(raw, pg * P + 128 * hf + 16 * g, n, st.scores + h * cap, st.page_stats + h * cap_chunks * 2,
-                    isd, j < G);
+          const size_t h = (size_t)u * G + 2 * (t & 1) + hh;
+          k5_finish(raw, pg * P + 128 * hfe + 16 * g, n, st.scores + h * cap, st.page_stats + h * cap_chunks * 2,
+                    isd, true);
         }
+      } else {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float raw[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              raw[2 * i] = acc[8 * hf + i][hh];
+              raw[2 * i + 1] = acc[8 * hf + i][2 + hh];
+            }
+            const int j = 2 * t + hh;
+            const size_t h = (size_t)u * G + (j < G ? j : 0);
+            k5_finish(raw, pg * P + 128 * hf + 16 * g, n, st.scores + h * cap, st.page_stats + h * cap_chunks * 2,
+                      isd, j < G);
+          }
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       cb = 0;
