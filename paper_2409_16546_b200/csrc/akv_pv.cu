@@ -394,21 +394,24 @@ struct PvCursor {
   UnitPages up;
 };
 
+// (unit, page, pass) advanced incrementally (no 64-bit division per page); the pages past
+// a unit's length are skipped as a block.
 template <int ROWS>
 __device__ __forceinline__ bool pv_cursor_seek(PvCursor& c, long long i1, const akv_store_t& s, int npg_max,
                                                int npass) {
-  for (; c.item < i1; ++c.item) {
-    const long long pi = c.item / npass;
-    const int u = (int)(pi / npg_max), pg = (int)(pi % npg_max);
-    if (u != c.up.u) unit_pages_fetch(c.up, s, u);
-    if (pg * P >= c.up.n) continue;
-    c.u = u;
-    c.pg = pg;
-    c.pass = (int)(c.item % npass);
-    c.rows = min(c.up.n - pg * P, P);
+  while (c.item < i1) {
+    if (c.u != c.up.u) unit_pages_fetch(c.up, s, c.u);
+    if (c.pg * P >= c.up.n) {
+      c.item += (long long)(npg_max - c.pg) * npass - c.pass;
+      c.pg = 0;
+      c.pass = 0;
+      ++c.u;
+      continue;
+    }
+    c.rows = min(c.up.n - c.pg * P, P);
     c.nsub = (c.rows + ROWS - 1) / ROWS;
     c.sub = 0;
-    c.pid = unit_page(c.up, s, pg);
+    c.pid = unit_page(c.up, s, c.pg);
     ++c.npage;
     return true;
   }
@@ -423,6 +426,13 @@ __device__ __forceinline__ bool pv_cursor_next(PvCursor& c, long long i1, const 
     return true;
   }
   ++c.item;
+  if (++c.pass == npass) {
+    c.pass = 0;
+    if (++c.pg == npg_max) {
+      c.pg = 0;
+      ++c.u;
+    }
+  }
   return pv_cursor_seek<ROWS>(c, i1, s, npg_max, npass);
 }
 
@@ -493,6 +503,9 @@ __global__ void __launch_bounds__(32 * Pv3Shape<G, UNIFORM>::WARPS, Pv3Shape<G, 
 
   PvCursor ic, cc;  // issue / consume cursors
   ic.item = i0;
+  ic.pass = (int)(i0 % S::NPASS);
+  ic.u = (int)(i0 / S::NPASS / npg_max);
+  ic.pg = (int)(i0 / S::NPASS % npg_max);
   ic.up.u = -1;
   ic.up.n = 0;
   ic.npage = 0;

@@ -400,11 +400,17 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
   up.u = -1;
   up.n = 0;
 
-  for (long long item = i0; item < i1; ++item) {
-    const int u = (int)(item / npg_max), pg = (int)(item % npg_max);
+  // (unit, page) walked incrementally (no 64-bit division per item); the pages past a
+  // unit's length are skipped as a block
+  int u = (int)(i0 / npg_max), pg = (int)(i0 % npg_max);
+  for (long long item = i0; item < i1; item = item + 1, pg = pg + 1 == npg_max ? 0 : pg + 1, u += pg == 0) {
     if (u != up.u) unit_pages_fetch(up, s, u);
     const int n = up.n;
-    if (pg * P >= n) continue;
+    if (pg * P >= n) {  // rest of this unit is past its length
+      item += npg_max - 1 - pg;
+      pg = npg_max - 1;
+      continue;
+    }
     if (ws.unit != u || pg == 0) k_prologue<G, TRUNC>(ws, s, cfg, st, u, n, pg == 0);
     const uint8_t* base = s.k_pool + unit_page(up, s, pg) * PAGE;
     const int nb8 = ws.n8p >> 3, nb = ws.nlist >> 3;
@@ -814,53 +820,68 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
   const long long i0 = total * gw / nw, i1 = total * (gw + 1) / nw;
   const int cap_chunks = s.max_pages * (P / 32);
 
-  // load cursor (li, lb) and compute cursor (ci, cb) over (item, slot); both walk the same items
+  // load cursor (l, lb) and compute cursor (c, cb) over (item, slot); both walk the same
+  // items, (unit, page) advanced incrementally (no 64-bit division per page)
+  struct Cur {
+    long long i;
+    int u, pg;
+  };
   UnitPages lup, cup;
   lup.u = cup.u = -1;
   lup.n = cup.n = 0;
-  auto seek = [&](long long i, UnitPages& up) -> long long {
-    for (; i < i1; ++i) {
-      const int u = (int)(i / npg_max), pg = (int)(i % npg_max);
-      if (u != up.u) unit_pages_fetch(up, s, u);
-      if (pg * P < up.n) return i;
+  auto seek = [&](Cur& c, UnitPages& up) {  // first valid item at or after c
+    while (c.i < i1) {
+      if (c.u != up.u) unit_pages_fetch(up, s, c.u);
+      if (c.pg * P < up.n) return;
+      c.i += npg_max - c.pg;  // the rest of this unit is past its length
+      c.pg = 0;
+      ++c.u;
     }
-    return i1;
   };
-  long long li = seek(i0, lup), ci = li;
+  auto advance = [&](Cur& c, UnitPages& up) {
+    ++c.i;
+    if (++c.pg == npg_max) {
+      c.pg = 0;
+      ++c.u;
+    }
+    seek(c, up);
+  };
+  Cur lc{i0, (int)(i0 / npg_max), (int)(i0 % npg_max)};
+  seek(lc, lup);
+  Cur cc = lc;
   cup = lup;
-  int lb = 0, cb = 0, issued = 0, computed = 0;
+  int lb = 0, cb = 0, issued = 0, computed = 0, islot = 0, cslot = 0;
   bool lblocked = false;  // the load cursor reached a unit whose lists are not built yet
   const uint8_t* lbase = nullptr;
-  if (li < i1) {
-    const int pg = (int)(li % npg_max);
-    k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, (int)(li / npg_max), lup.n, pg == 0);
-    lbase = s.k_pool + unit_page(lup, s, pg) * PAGE;
+  if (lc.i < i1) {
+    k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, lc.u, lup.n, lc.pg == 0);
+    lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
   }
   float acc[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
-  while (ci < i1) {
+  while (cc.i < i1) {
     const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
     // issue up to NB-1 slots ahead (stop at a unit whose lists are not built)
-    while (li < i1 && !lblocked && issued - computed < NB - 1) {
-      q5_issue<G>(ring + (issued % NB) * Q5_SLOT, ws, lb, lbase);
+    while (lc.i < i1 && !lblocked && issued - computed < NB - 1) {
+      q5_issue<G>(ring + islot * Q5_SLOT, ws, lb, lbase);
       ++issued;
+      islot = islot + 1 == NB ? 0 : islot + 1;
       if (++lb == nslots) {
         lb = 0;
-        const long long pu = li / npg_max;
-        li = seek(li + 1, lup);
-        if (li < i1) {
-          if (li / npg_max != pu) lblocked = true;  // new unit: wait for the math to drain
-          else lbase = s.k_pool + unit_page(lup, s, (int)(li % npg_max)) * PAGE;
+        const int pu = lc.u;
+        advance(lc, lup);
+        if (lc.i < i1) {
+          if (lc.u != pu) lblocked = true;  // new unit: wait for the math to drain
+          else lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
         }
       }
     }
     if (issued == computed) {
       // drained at a unit boundary: build the next unit's lists, resume loading
-      const int pg = (int)(li % npg_max);
-      k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, (int)(li / npg_max), lup.n, pg == 0);
-      lbase = s.k_pool + unit_page(lup, s, pg) * PAGE;
+      k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, lc.u, lup.n, lc.pg == 0);
+      lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
       lblocked = false;
       continue;
     }
@@ -870,14 +891,14 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
     else if (inflight == 2) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncwarp();
-    q5_compute<G, TRUNC>(ring + (computed % NB) * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
+    q5_compute<G, TRUNC>(ring + cslot * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
     ++computed;
+    cslot = cslot + 1 == NB ? 0 : cslot + 1;
     __syncwarp();  // every lane is done with the slot before it is refilled
     if (++cb == nslots) {
       // page done: lane (g, t) holds tokens 16g + 2i (acc[i][0..1]) and 16g + 2i + 1
       // (acc[i][2..3]) of each page half for heads 2t, 2t+1
-      const int u = (int)(ci / npg_max), pg = (int)(ci % npg_max);
-      if (u != cup.u) unit_pages_fetch(cup, s, u);
+      const int u = cc.u, pg = cc.pg;
       const int n = cup.n;
       if (G == 4) {
         // heads 4..7 are padding: lanes t >= 2 take over page half 1 of lane t - 2, so
@@ -923,7 +944,7 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       cb = 0;
-      ci = seek(ci + 1, cup);
+      advance(cc, cup);
     }
   }
 }
@@ -956,24 +977,24 @@ static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
                         cudaStream_t stream) {
   if constexpr (G >= 4) {
     launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
-    return;
+  } else {
+    static int resident = 0;
+    const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
+    if (!resident) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(qk_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk_kernel<G, TRUNC>, 32 * QK_WARPS, smem);
+      resident = sms * std::max(per, 1);
+    }
+    const int cap = s.max_pages * P;
+    const int npg = (max_len + P - 1) / P;
+    const long long items = (long long)s.n_units * npg;
+    const int grid = (int)std::min<long long>(resident, std::max<long long>((items + QK_WARPS - 1) / QK_WARPS, 1));
+    const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
+    launch_pdl(qk_kernel<G, TRUNC>, dim3(grid), dim3(32 * QK_WARPS), smem, stream, s, cfg, st, cap, isd, npg);
   }
-  static int resident = 0;
-  const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
-  if (!resident) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(qk_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk_kernel<G, TRUNC>, 32 * QK_WARPS, smem);
-    resident = sms * std::max(per, 1);
-  }
-  const int cap = s.max_pages * P;
-  const int npg = (max_len + P - 1) / P;
-  const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + QK_WARPS - 1) / QK_WARPS, 1));
-  const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  launch_pdl(qk_kernel<G, TRUNC>, dim3(grid), dim3(32 * QK_WARPS), smem, stream, s, cfg, st, cap, isd, npg);
 }
 
 void launch_qk(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len, cudaStream_t stream) {
