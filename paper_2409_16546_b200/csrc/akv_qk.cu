@@ -770,10 +770,17 @@ __device__ __forceinline__ void k5_finish(const float (&raw)[16], int tok0, int 
     if (e < nv) m = fmaxf(m, sv[e]);
   }
   m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 4));
+  // sum of exp(s - m) <= 32 terms, the largest exactly 1: the MUFU exp2 (rel. error ~2^-22
+  // per term) moves the chunk's sum, and so L and every p, by ~1e-7 relative
+  const float ml = m * 1.4426950408889634f;
   float l = 0.f;
 #pragma unroll
   for (int e = 0; e < 16; ++e)
-    if (e < nv) l += expf(sv[e] - m);
+    if (e < nv) {
+      float ex;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(fmaf(sv[e], 1.4426950408889634f, -ml)));
+      l += ex;
+    }
   l += __shfl_xor_sync(0xFFFFFFFFu, l, 4);
   if (!store) return;  // (lanes of absent heads: the shuffles above need the whole warp)
   float* out = scores_h + tok0;
