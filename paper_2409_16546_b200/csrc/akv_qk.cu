@@ -347,10 +347,14 @@ __device__ __forceinline__ void qk_finish(const float* raw, int tok0, int n, flo
   }
   m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
   m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 16));
-  float l = 0.f;
+  float l = 0.f;  // MUFU exp2 of (s - m) log2(e), as in k5_finish
 #pragma unroll
   for (int e = 0; e < 8; ++e)
-    if (e < nv) l += expf(sv[e] - m);
+    if (e < nv) {
+      float ex;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"((sv[e] - m) * 1.4426950408889634f));
+      l += ex;
+    }
   l += __shfl_xor_sync(0xFFFFFFFFu, l, 1);
   l += __shfl_xor_sync(0xFFFFFFFFu, l, 16);
   float* out = scores_h + tok0;
@@ -770,15 +774,15 @@ __device__ __forceinline__ void k5_finish(const float (&raw)[16], int tok0, int 
     if (e < nv) m = fmaxf(m, sv[e]);
   }
   m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, 4));
-  // sum of exp(s - m) <= 32 terms, the largest exactly 1: the MUFU exp2 (rel. error ~2^-22
-  // per term) moves the chunk's sum, and so L and every p, by ~1e-7 relative
-  const float ml = m * 1.4426950408889634f;
+  // sum of exp(s - m) over <= 32 terms by the MUFU exp2 (rel. error ~2^-22 per term: L and
+  // every p move by ~1e-7 relative).  s - m is formed first so the maximum term is exactly
+  // ex2(0) = 1 (a one-hot softmax stays exactly one-hot).
   float l = 0.f;
 #pragma unroll
   for (int e = 0; e < 16; ++e)
     if (e < nv) {
       float ex;
-      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(fmaf(sv[e], 1.4426950408889634f, -ml)));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"((sv[e] - m) * 1.4426950408889634f));
       l += ex;
     }
   l += __shfl_xor_sync(0xFFFFFFFFu, l, 4);

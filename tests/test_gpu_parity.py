@@ -226,6 +226,11 @@ def test_spec_examples_embedded():
     st2.append(torch.from_numpy(K.view(np.int16)), torch.from_numpy(V.view(np.int16)))
     r = AD.decode_step(torch.from_numpy(q.view(np.int16)), st2)
     assert np.array_equal(r.o[0, 0].cpu().numpy(), ohb.decode_array(V[1]).astype(np.float32))
+    # ... and through the GQA kernels (4 q-heads on the kv-head)
+    q4 = np.tile(q, (4, 1)).reshape(1, 4, 128)
+    r4 = AD.decode_step(torch.from_numpy(q4.view(np.int16)), st2)
+    for j in range(4):
+        assert np.array_equal(r4.o[0, j].cpu().numpy(), ohb.decode_array(V[1]).astype(np.float32))
 
 
 def test_error_histograms_match_oracle():
