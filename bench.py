@@ -308,12 +308,14 @@ def main():
         step(cfg_aligned)
     for _ in range(args.warmup):
         step(cfg_control)
+    # clocks sampled from the start of the timed region through the control and breakdown
+    # runs that follow it (the K-step region alone is a few ms: one or two NVML samples)
     clocks = Clocks(local)
     ms = timed(cfg_aligned, args.steps)
-    clk = clocks.stop()
     ms_ctl = timed(cfg_control, args.steps)
     bd = breakdown(cfg_aligned, args.steps)
     bd_ctl = breakdown(cfg_control, max(3, args.steps // 2))
+    clk = clocks.stop()
 
     # ---- counters of the aligned step -> bytes, bit widths
     step(cfg_aligned)
