@@ -1,10 +1,11 @@
 // softmax + estimate_output (D3) +
 // rule2_targets for every (unit, q-head): one CTA each.
 //
-//  1. combine the per-page (max, sum exp) of the QK kernel -> M, L;
-//  2. p_t = exp(s_t - M) / L (written to probs, may overwrite scores in
-//     place); tokens with p_t >= pmax * 2^-m are compacted into a shared
-//     candidate list (warp-aggregated atomics);
+//  1. combine the per-32-token-chunk (max, sum exp) of the QK kernel -> M, L;
+//  2. p_t = exp(s_t - M) * (1/L) (written to probs); tokens with
+//     p_t >= pmax * 2^-m are compacted into a shared candidate list
+//     (warp-aggregated atomics); with 256-thread CTAs (contexts <= 8k) the
+//     per-token fetch-plan bound of step 6 is computed here as well;
 //  3. |C| <= k_sel: the selection is C.  Otherwise the k_sel largest by
 //     (p desc, t asc): an exact 4-pass radix select on the fp32 bit patterns
 //     of the candidates (p >= 0, so bit order = value order), ties at the
@@ -12,7 +13,9 @@
 //  4. the selection is sorted by t; o_est = sum_{t in sel} p_t * V[t] at T16
 //     (warps split the rows, fixed-order reduction);
 //  5. target_r = floor(log2|o_est_r|) - 10 (0 -> unknown) plus the minimum
-//     known target and an any-unknown flag for the PV superset rule (H6).
+//     known target and an any-unknown flag for the PV superset rule (H6);
+//  6. the PV fetch plan: per-row need-mid / need-low bitmaps.
+// CTA size: 256 threads up to 8k tokens, 512 above (launch_select).
 #include "akv_common.cuh"
 
 namespace akv {
