@@ -872,10 +872,12 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
-  while (cc.i < i1) {
-    const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
-    // issue up to NB-1 slots ahead (stop at a unit whose lists are not built)
-    while (lc.i < i1 && !lblocked && issued - computed < NB - 1) {
+  // One cp.async group is committed per step (an empty one when the load cursor waits at a
+  // unit boundary), so the slot about to be computed always has NB-2 groups after it and a
+  // constant wait_group<NB-2> suffices.
+  auto issue_one = [&]() {
+    if (lc.i < i1 && !lblocked) {
+      const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
       q5_issue<G>(ring + islot * Q5_SLOT, ws, lb, lbase);
       ++issued;
       islot = islot + 1 == NB ? 0 : islot + 1;
@@ -888,24 +890,30 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
           else lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
         }
       }
+    } else {
+      cp_async_commit();
     }
+  };
+#pragma unroll 1
+  for (int k = 0; k < NB - 1; ++k) issue_one();
+  while (cc.i < i1) {
+    const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
     if (issued == computed) {
-      // drained at a unit boundary: build the next unit's lists, resume loading
+      // drained at a unit boundary: build the next unit's lists, refill the ring
       k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, lc.u, lup.n, lc.pg == 0);
       lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
       lblocked = false;
+#pragma unroll 1
+      for (int k = 0; k < NB - 1; ++k) issue_one();
       continue;
     }
-    const int inflight = issued - computed;  // 1 .. NB-1
-    if (inflight >= 4) cp_async_wait<3>();
-    else if (inflight == 3) cp_async_wait<2>();
-    else if (inflight == 2) cp_async_wait<1>();
-    else cp_async_wait<0>();
+    cp_async_wait<NB - 2>();
     __syncwarp();
     q5_compute<G, TRUNC>(ring + cslot * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
     ++computed;
     cslot = cslot + 1 == NB ? 0 : cslot + 1;
     __syncwarp();  // every lane is done with the slot before it is refilled
+    issue_one();
     if (++cb == nslots) {
       // page done: lane (g, t) holds tokens 16g + 2i (acc[i][0..1]) and 16g + 2i + 1
       // (acc[i][2..3]) of each page half for heads 2t, 2t+1
