@@ -346,3 +346,21 @@ def test_gqa_long_context():
     """g = 8 over 40 pages (n > 8192: the 1024-thread select; qk5 rings continuous across
     many pages of a unit; pv quad path)."""
     _compare_case(Case(B=1, Hkv=1, g=8, n=10000, seed=17))
+
+
+@pytest.mark.parametrize("g,n,lo,hi", [(1, 1500, -4.0, 4.0), (2, 700, -0.5, 0.5), (4, 1500, -4.0, 4.0),
+                                       (4, 700, -0.5, 0.5), (8, 600, -4.0, 4.0)])
+def test_fast_path_parity(g, n, lo, hi):
+    """The serving path (no v-tier export: pv stage fast path, and for g >= 4 the quad path)
+    against the oracle; the other parity tests export the V tier masks, which runs the
+    per-batch path instead."""
+    c = Case(B=2, Hkv=2, g=g, n=n, seed=60 + g, lo=lo, hi=hi)
+    r = AD.decode_step(c.q, c.store)
+    o = r.o.cpu().numpy()
+    cnt = r.counters.cpu().numpy()
+    ref_e = c.gpu()  # export run: exact V-side counters for comparison
+    cnt_e = ref_e.counters.cpu().numpy()
+    for u, b, hq, j in c.units():
+        ref = c.oracle(u, j)
+        assert close(o[b, hq], ref.o), (g, u, j)
+    assert np.array_equal(cnt, cnt_e)  # same tier decisions -> same element counts
