@@ -364,3 +364,22 @@ def test_fast_path_parity(g, n, lo, hi):
         ref = c.oracle(u, j)
         assert close(o[b, hq], ref.o), (g, u, j)
     assert np.array_equal(cnt, cnt_e)  # same tier decisions -> same element counts
+
+
+def test_decode_graph_gqa_matches_eager():
+    """DecodeGraph (CUDA graph: append + qk5 + select + pv quad path + combine) with g = 4
+    equals the eager step bit for bit."""
+    B, Hkv, g, n, d = 1, 2, 4, 700, 128
+    K, V, Q = generate_batch(B, Hkv, n, d, g, 12)
+    kt = torch.from_numpy(K.view(np.int16)).view(B, Hkv, n, d)
+    vt = torch.from_numpy(V.view(np.int16)).view(B, Hkv, n, d)
+    q = torch.from_numpy(Q.view(np.int16)).view(B, Hkv * g, d)
+    a = KVStore(B, Hkv, d, 1024)
+    a.append(kt, vt)
+    ref = AD.decode_step(q, a)
+    b = KVStore(B, Hkv, d, 1024)
+    b.append(kt[:, :, : n - 1], vt[:, :, : n - 1])
+    dg = AD.DecodeGraph(b, g, rewind_to=n - 1).capture()
+    for _ in range(2):  # replays rewind and re-append the same token
+        out = dg.step(q, kt[:, :, n - 1], vt[:, :, n - 1])
+        assert torch.equal(out, ref.o.cpu().view_as(out))
