@@ -123,7 +123,11 @@ int64_t akv_workspace_bytes(int32_t n_units, int32_t group, int32_t max_pages);
 int akv_step_carve(akv_step_t* step, void* workspace, int32_t n_units, int32_t group, int32_t max_pages);
 
 /* Append n_new tokens per unit: k,v [U][n_new][d] fp16 bits.  status [U].
- * Non-finite input rejects that unit's whole append (length unchanged). */
+ * Non-finite input or a full page table rejects that unit's whole append
+ * (length unchanged).  Status words are sticky: the kernels write only error
+ * codes, keep the first one, and a multi-token append refuses a unit whose
+ * word is already non-zero; the caller zeroes status before an append whose
+ * outcome it reads (KVStore.append does), so errors survive graph replays. */
 int akv_append(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t n_new,
                int64_t* status, void* stream);
 

@@ -86,7 +86,8 @@ def estimate_output(p, store: KVStore, k_sel: int = 32, m: int = 5):
 def v_element_codes(p, sel, targets, known, v_head, cfg: AlignConfig = AlignConfig()) -> np.ndarray:
     """Per-element V read codes [n, d] for the element strategy.
 
-    target unknown -> 16 (SPEC.md:169); p_t == 0 -> 8 (D5);
+    target unknown -> 16 ("force tier T16 for reads contributing to
+    them", applied after and therefore over the p_t == 0 rule); p_t == 0 -> 8 (D5);
     e_v = max(bexp,1) - 15 from the head byte (D4); selected rows -> 16 (D6).
     Usable with the GPU's own p/sel/targets (injection check, D11).
     """

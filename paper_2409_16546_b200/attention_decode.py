@@ -503,9 +503,14 @@ class DecodeGraph:
             st._host_len += 1
 
     def step(self, q=None, k_new=None, v_new=None) -> torch.Tensor:
-        """Optionally copy q / k_new / v_new into the pinned host buffers, replay, return host o."""
+        """Optionally copy q / k_new / v_new into the pinned host buffers, replay, return host o.
+
+        Refuses to replay when the append would exceed the store's capacity (the device would
+        reject it and the output would silently be stale)."""
         if self.graph is None:
             self.capture()
+        if self.rewind_to is None and int(self.store._host_len.max()) + 1 > self.store.capacity:
+            raise ValueError(f"store is full ({self.store.capacity} tokens): cannot append another token")
         for src, dst in ((q, self.host_q), (k_new, self.host_k), (v_new, self.host_v)):
             if src is not None:
                 dst.copy_(_as_bits(src, torch.device("cpu")).view(dst.shape))
@@ -515,13 +520,19 @@ class DecodeGraph:
         return self.host_o
 
     def check(self):
-        """Raise the device-side status of the last replay (non-finite K/V, degenerate q)."""
+        """Raise the device-side status of the replays since the last check (non-finite K/V,
+        capacity, degenerate q).  Append errors are sticky on device, so a rejection in any
+        replay is reported; the host length mirror is resynchronised from the device and the
+        status words are cleared so the graph can keep serving."""
         st = self.store
         s = st.status_dev.cpu().numpy()
         bad = np.nonzero(s)[0]
         if bad.size:
+            st._host_len[:] = st.lengths_dev.cpu().numpy()
+            st.status_dev.zero_()
             code, isv, c, t = decode_status(int(s[bad[0]]))
             b, h = divmod(int(bad[0]), st.n_kv_heads)
-            raise ValueError(f"append failed: status code {code} ({'V' if isv else 'K'}) at batch {b}, "
-                             f"kv-head {h}, channel {c}")
+            what = {_lib.STATUS_NONFINITE: f"non-finite {'V' if isv else 'K'} channel {c}",
+                    _lib.STATUS_CAPACITY: "capacity exceeded"}.get(code, f"status code {code}")
+            raise ValueError(f"append failed ({what}) at batch {b}, kv-head {h}")
         _raise_status(self.ws, st)

@@ -32,15 +32,17 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   if (!finite16(vw)) atomicMin(&s_bad, 0x100 | c);
   atomicMax(&s_rowmax, vw & 0x7FFFu);
   __syncthreads();
+  // status words are sticky: only errors are written, and the first one stays until the
+  // caller clears the word (a replayed CUDA graph cannot lose a rejected append)
   if (s_bad != 0x7FFFFFFF) {
-    if (c == 0) {
+    if (c == 0 && status[u] == 0) {
       const int bad = s_bad;
       status[u] = status_word(AKV_STATUS_NONFINITE, ((long long)(bad >> 8) << 59) | ((long long)(bad & 0xFF) << 40));
     }
     return;
   }
   if (!room) {
-    if (c == 0) status[u] = status_word(AKV_STATUS_CAPACITY, t);
+    if (c == 0 && status[u] == 0) status[u] = status_word(AKV_STATUS_CAPACITY, t);
     return;
   }
   const int tt = t % P;
@@ -79,7 +81,6 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   // sidecars: ColMax by reduction, RowMax from the block max
   atomicMax(s.colmax + (size_t)u * D + c, kw & 0x7FFFu);
   if (c == 0) {
-    status[u] = 0;
     s.rowmax[(size_t)u * s.max_pages * P + t] = (uint16_t)s_rowmax;
     s.lengths[u] = t + 1;
   }
@@ -110,13 +111,13 @@ __global__ void __launch_bounds__(256) append_validate_kernel(akv_store_t s, con
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = min(best, s_best[w]);
     const int t0 = s.lengths[u];
-    if (best != 0x7FFFFFFFFFFFFFFFLL) {
+    if (status[u] != 0) {
+      // an earlier rejection is still pending (sticky): this append is refused too
+    } else if (best != 0x7FFFFFFFFFFFFFFFLL) {
       const long long t = best >> 9, isv = (best >> 8) & 1, c = best & 0xFF;
       status[u] = status_word(AKV_STATUS_NONFINITE, (isv << 59) | (c << 40) | t);
     } else if ((long long)t0 + n_new > (long long)s.max_pages * P) {
       status[u] = status_word(AKV_STATUS_CAPACITY, t0);
-    } else {
-      status[u] = 0;
     }
   }
 }

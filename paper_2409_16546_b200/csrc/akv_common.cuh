@@ -227,6 +227,27 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&lc, kernel, args...);
 }
 
+// Resident CTAs of a kernel across the current device (SMs x occupancy), with the
+// dynamic shared-memory opt-in applied.  Both are per-device properties, so the
+// cache is keyed by the device ordinal (one process may drive several GPUs);
+// computing an entry twice under a race is harmless (idempotent).
+constexpr int MAX_DEVICES = 64;
+template <auto Kern>
+inline int resident_ctas(int threads, size_t smem) {
+  static int cache[MAX_DEVICES] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int* slot = dev >= 0 && dev < MAX_DEVICES ? &cache[dev] : nullptr;
+  if (slot && *slot) return *slot;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, Kern, threads, smem);
+  const int r = sms * (per > 0 ? per : 1);
+  if (slot) *slot = r;
+  return r;
+}
+
 __device__ __forceinline__ long long status_word(long long code, long long pos) { return (code << 60) | pos; }
 
 __device__ __forceinline__ const uint8_t* page_ptr(const uint8_t* pool, const int32_t* table, int max_pages, int u,

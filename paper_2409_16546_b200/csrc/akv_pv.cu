@@ -16,7 +16,8 @@
 // fp32 by HADD2.F32, p_t * V~ by the packed FFMA2 into fp32.
 // Selected rows carry p = 0 here (D6: their T16 contribution is o_est).
 // Other rows fetch the needed 64 B nibble rows (LDG) and apply each q-head's
-// rule: p_t = 0 -> T8 (D5); ELEMENT: keep mid iff max(bexp,1) + e(p_t) >
+// rule: unknown target_r -> T16 (p_t = 0 included), else p_t = 0 -> T8 (D5);
+// ELEMENT: keep mid iff max(bexp,1) + e(p_t) >
 // 17 + target_r - margin, low iff > that + 4 (D4); row strategy: the row tier
 // (D7); forced / baseline tiers.  Truncation is applied after the fetch, so
 // the masks equal the oracle's bit for bit.  The page's partial output goes to
@@ -87,7 +88,7 @@ __device__ __forceinline__ void v_row_generic(VGen<HG>& out, const uint4& hv, ui
     } else {
       const uint32_t nm = st.need_bits[h * 2 * capw + c.pg * 8 + ch];
       if (!((nm >> (row & 31)) & 1u)) {
-        mode = 8;  // includes p == 0 (D5)
+        mode = 8;  // p == 0 rows are outside the plan unless some target is unknown (D5)
       } else if (cfg.strategy == 1) {
         const uint32_t nl = st.need_bits[h * 2 * capw + capw + c.pg * 8 + ch];
         mode = ((nl >> (row & 31)) & 1u) ? 16 : 12;
@@ -770,15 +771,7 @@ template <int G, bool TRUNC, bool EXPORT, bool UNIFORM>
 static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
   using S = Pv3Shape<G, UNIFORM>;
-  static int resident = 0;
-  if (!resident) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, 32 * S::WARPS, S::SMEM);
-    resident = sms * std::max(per, 1);
-  }
+  const int resident = resident_ctas<pv3_kernel<G, TRUNC, EXPORT, UNIFORM>>(32 * S::WARPS, S::SMEM);
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg * S::NPASS;

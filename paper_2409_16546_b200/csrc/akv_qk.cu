@@ -972,15 +972,7 @@ template <int G, bool TRUNC>
 static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
   using S = Qk5Shape<G>;
-  static int resident = 0;
-  if (!resident) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(qk5_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk5_kernel<G, TRUNC>, 32 * S::WARPS, S::SMEM);
-    resident = sms * std::max(per, 1);
-  }
+  const int resident = resident_ctas<qk5_kernel<G, TRUNC>>(32 * S::WARPS, S::SMEM);
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
@@ -997,16 +989,8 @@ static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
   if constexpr (G >= 4) {
     launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
   } else {
-    static int resident = 0;
     const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
-    if (!resident) {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaFuncSetAttribute(qk_kernel<G, TRUNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qk_kernel<G, TRUNC>, 32 * QK_WARPS, smem);
-      resident = sms * std::max(per, 1);
-    }
+    const int resident = resident_ctas<qk_kernel<G, TRUNC>>(32 * QK_WARPS, smem);
     const int cap = s.max_pages * P;
     const int npg = (max_len + P - 1) / P;
     const long long items = (long long)s.n_units * npg;

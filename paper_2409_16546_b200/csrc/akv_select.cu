@@ -386,9 +386,11 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 2) select_kernel(akv_store
             nm = x - tmin_all > 2;
             nlw = x - tmin_all > 6;
           }
-        } else if (x != XS_P0) {
-          nm = unk_all || x - tmin_all > 2;
-          nlw = unk_all || x - tmin_all > 6;
+        } else {
+          // an unknown target (o_est_r == 0) forces T16 on every read contributing to that
+          // dim, p_t == 0 included (Appendix A D5 as amended in DESIGN §4)
+          nm = unk_all || (x != XS_P0 && x - tmin_all > 2);
+          nlw = unk_all || (x != XS_P0 && x - tmin_all > 6);
         }
       }
       const uint32_t sw = sm.selw[w];
@@ -430,10 +432,10 @@ __global__ void __launch_bounds__(ST, ST == 256 ? 4 : 2) select_kernel(akv_store
             }
             nm = tier >= 12;
             nlw = tier == 16;
-          } else if (!sel && p > 0.f) {
+          } else if (!sel) {
             if (unk_all) {
-              nm = nlw = true;
-            } else {
+              nm = nlw = true;  // SPEC.md:169, p_t == 0 included
+            } else if (p > 0.f) {
               const int bound = floor_log2f(p) + (max(bexp16(rm), 1) - 15) + 1 - tmin_all - 1 + cfg.margin_bits;
               nm = bound > 2;
               nlw = bound > 6;

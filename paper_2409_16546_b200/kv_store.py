@@ -197,6 +197,7 @@ class KVStore:
             return
         if int(self._host_len.max()) + T > self.capacity:
             raise ValueError(f"append of {T} tokens exceeds capacity {self.capacity}")
+        self.status_dev.zero_()  # status words are sticky (akv.h): clear before an append whose outcome we read
         rc = self._L.akv_append(ctypes.byref(self.c_store), k.data_ptr(), v.data_ptr(), T,
                                 self.status_dev.data_ptr(), self._stream())
         _lib.check(rc, "akv_append")
@@ -237,6 +238,25 @@ class KVStore:
             raise ValueError("rewind can only shorten")
         self.lengths_dev.fill_(n_tokens)
         self._host_len[:] = n_tokens
+
+    def batch_prefix(self, batch: int) -> "KVStore":
+        """A store over the first `batch` batch rows that shares every device buffer of this
+        one (units are b-major, so the prefix is contiguous); used by the batch sweep."""
+        if not 1 <= batch <= self.batch:
+            raise ValueError(f"batch prefix {batch} outside [1, {self.batch}]")
+        v = object.__new__(KVStore)
+        v.__dict__.update(self.__dict__)
+        U = batch * self.n_kv_heads
+        v.batch = batch
+        v._host_len = self._host_len[:U]
+        for name in ("page_table", "lengths_dev", "colmax_dev", "rowmax_dev", "status_dev"):
+            setattr(v, name, getattr(self, name)[:U])
+        v._pending = None
+        v._workspaces = {}
+        v.c_store = _lib.AkvStore(U, self.n_dims, self.max_pages, 0, self.k_pool.data_ptr(), self.v_pool.data_ptr(),
+                                  v.page_table.data_ptr(), v.lengths_dev.data_ptr(), v.colmax_dev.data_ptr(),
+                                  v.rowmax_dev.data_ptr())
+        return v
 
     # ---------------------------------------------------------------- sidecars / export
     def colmax(self) -> torch.Tensor:

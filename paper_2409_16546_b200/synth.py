@@ -62,3 +62,17 @@ def generate_batch(batch: int, n_kv: int, n: int, d: int = 128, g: int = 1, seed
     for w, (k, v, q) in enumerate(parts):
         K[w::workers], V[w::workers], Q[w::workers] = k, v, q
     return K, V, Q
+
+
+def fill_store(store, K, V, n_tokens: int, chunk: int = 1024) -> None:
+    """Bulk-append tokens [0, n_tokens) of every unit (K, V [U, >=n_tokens, d] uint16) into a
+    GPU KVStore in chunks, bounding the host->device staging; raises on non-finite input."""
+    import torch
+
+    B, H, d = store.batch, store.n_kv_heads, store.n_dims
+    for t0 in range(0, n_tokens, chunk):
+        t1 = min(n_tokens, t0 + chunk)
+        kt = torch.from_numpy(np.ascontiguousarray(K[:, t0:t1]).view(np.int16)).view(B, H, t1 - t0, d)
+        vt = torch.from_numpy(np.ascontiguousarray(V[:, t0:t1]).view(np.int16)).view(B, H, t1 - t0, d)
+        store.append(kt, vt)
+    store.check()

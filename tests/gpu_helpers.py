@@ -9,25 +9,20 @@ import torch
 from oracle import attention_decode as OA
 from oracle.align_core import AlignConfig as OAlignConfig
 from oracle.kv_store import KVStore as OStore
+from oracle.parity import check_head, close  # noqa: F401  (re-exported for the tests)
 from paper_2409_16546_b200 import AlignConfig, KVStore
 from paper_2409_16546_b200.attention_decode import decode_step
 from paper_2409_16546_b200.synth import generate_batch
 
 
-def close(gpu, ref, rtol=1e-3):
-    """|gpu - ref| <= rtol*|ref| + rtol*max|ref| (per vector)."""
-    gpu = np.asarray(gpu, np.float64)
-    ref = np.asarray(ref, np.float64)
-    tol = rtol * np.abs(ref) + rtol * np.max(np.abs(ref), axis=-1, keepdims=True)
-    return np.all(np.abs(gpu - ref) <= tol + 1e-30)
-
-
 class Case:
     """B x Hkv units with n tokens (n-1 bulk + 1 appended), g q-heads per kv-head."""
 
-    def __init__(self, B=2, Hkv=2, g=1, n=300, seed=11, lo=-4.0, hi=4.0, capacity=None):
+    def __init__(self, B=2, Hkv=2, g=1, n=300, seed=11, lo=-4.0, hi=4.0, capacity=None, mutate=None):
         self.B, self.Hkv, self.g, self.n = B, Hkv, g, n
         K, V, Q = generate_batch(B, Hkv, n, 128, g, seed, lo, hi)
+        if mutate is not None:  # edit the synthetic units in place before they are stored
+            mutate(K, V, Q)
         self.K, self.V, self.Q = K, V, Q  # [U,n,d], [U,n,d], [U,g,d]
         cap = capacity or max(256, n)
         self.store = KVStore(B, Hkv, 128, cap)

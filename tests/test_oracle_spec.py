@@ -207,3 +207,20 @@ def test_acceptance4_5_statistics():
     assert np.mean(hq, 0)[0] > np.mean(hb13q, 0)[0]
     assert np.mean(hsv, 0)[0] > np.mean(hb13sv, 0)[0]
     assert np.mean(hsv, 0)[5] <= 0.02
+
+
+def test_unknown_target_wins_over_p_zero():
+    """SPEC.md:169 over D5: an unknown Rule-2 target forces T16 even where p_t == 0; known
+    dims keep the p_t == 0 -> T8 rule; selected rows are T16 (D6)."""
+    import numpy as np
+
+    from oracle.attention_decode import v_element_codes
+
+    p = np.array([0.0, 0.5, 0.5])
+    targets = np.array([-10, 0])
+    known = np.array([True, False])
+    v_head = np.full((3, 2), 0x3C, np.int64)  # 1.0
+    codes = v_element_codes(p, np.array([1]), targets, known, v_head)
+    assert codes[0].tolist() == [8, 16]
+    assert codes[1].tolist() == [16, 16]
+    assert codes[2, 1] == 16
