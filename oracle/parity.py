@@ -40,8 +40,9 @@ def check_head(ref: "OA.HeadResult", *, k_tiers, o, counters, sel=None, v_tiers=
                force=None):
     """Compare one q-head's GPU outputs with the oracle's HeadResult.
 
-    Returns (failures: list[str], knife_edge: bool).  Optional arguments that
-    are None are not checked (e.g. the serving path exports no V mask).
+    Returns (failures: list[str], knife_edge: bool) — knife_edge is True when any
+    D11 exclusion applied (a selection edge, or excluded rows / columns).  Optional
+    arguments that are None are not checked (the serving path exports no V mask).
     """
     fail = []
     counters = np.asarray(counters)
@@ -57,6 +58,11 @@ def check_head(ref: "OA.HeadResult", *, k_tiers, o, counters, sel=None, v_tiers=
     d = ref.k_tiers.shape[0]
     if force is None:
         rows, cols, edge = OA.knife_edges(ref.p, ref.o_est, ref.sel)
+        # a selected row is read at T16 whatever its p (D6): no decision sits on its edge
+        # (the argmax of a one-hot softmax has p = 1.0 exactly, log2 p = 0)
+        rows[np.asarray(ref.sel, dtype=np.int64)] = False
+        if strategy == "element" and v_head is not None and (rows.any() or cols.any()):
+            rows, cols = _flipping(ref, rows, cols, v_head, cfg)
     else:
         rows, cols, edge = np.zeros(n, bool), np.zeros(d, bool), False
     if sel is not None and not edge and not np.array_equal(np.asarray(sel), ref.sel):
@@ -78,3 +84,34 @@ def check_head(ref: "OA.HeadResult", *, k_tiers, o, counters, sel=None, v_tiers=
         if tuple(int(x) for x in counters[3:6]) != ref.v_counter.as_tuple():
             fail.append("v_counter")
     return fail, bool(edge or rows.any() or cols.any())
+
+
+def _flipping(ref, rows, cols, v_head, cfg):
+    """Keep only the knife-edge rows / columns whose V tiers actually change when the
+    float-derived exponent (e(p_t) per row, the Rule-2 target per column) is read one
+    lower or one higher; an edge that cannot flip a tier is no ambiguity (e.g. a p_t of
+    1e-61 sits at e(p) = -201 +- 1: T8 either way)."""
+    from oracle.align_core import rule2_targets_array
+
+    tg, known = rule2_targets_array(ref.o_est)
+    base = OA.v_element_codes(ref.p, ref.sel, tg, known, v_head, cfg)
+    keep_r = np.zeros_like(rows)
+    if rows.any():
+        for f in (2.0, 0.5):
+            pp = ref.p.copy()
+            pp[rows] *= f
+            keep_r |= rows & (OA.v_element_codes(pp, ref.sel, tg, known, v_head, cfg) != base).any(axis=1)
+    keep_c = np.zeros_like(cols)
+    if cols.any():
+        for dlt in (1, -1):
+            t2 = np.asarray(tg).copy()
+            t2[cols] += dlt
+            keep_c |= cols & (OA.v_element_codes(ref.p, ref.sel, t2, known, v_head, cfg) != base).any(axis=0)
+    return keep_r, keep_c
+
+
+def knife_edge_kind(ref: "OA.HeadResult"):
+    """(selection_edge, excluded_rows, excluded_cols) of one head under D11, for reporting."""
+    rows, cols, edge = OA.knife_edges(ref.p, ref.o_est, ref.sel)
+    rows[np.asarray(ref.sel, dtype=np.int64)] = False
+    return bool(edge), int(rows.sum()), int(cols.sum())

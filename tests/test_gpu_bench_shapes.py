@@ -64,7 +64,7 @@ def test_bench_shape_parity(name):
 
     # sampled units in full
     o_srv = srv.o.cpu().numpy()
-    edges = 0
+    edges = heads = 0
     for u in sample:
         b, h = divmod(u, Hkv)
         ost = OStore(d)
@@ -80,4 +80,5 @@ def test_bench_shape_parity(name):
             assert not fail, (name, u, j, fail)
             assert close(o_srv[b, hq], ref.o), (name, u, j)
             edges += edge
-    assert edges <= 1, edges
+            heads += 1
+    assert edges <= max(1, heads // 4), f"{edges} knife-edge heads of {heads}"
