@@ -114,13 +114,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 // Watchdog: a protocol bug must fail the launch (trap -> cudaErrorLaunchFailure),
-// never hang the GPU.  try_wait suspends for a hardware time slice per call,
-// so 2^26 failed polls is tens of seconds.
+// never hang the GPU: a wait longer than 2 s of wall time traps.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins == (1u << 26)) __trap();
+    if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 2000000000ull) __trap();
   }
 }
 // Bulk global -> shared copy completing on an mbarrier (bytes % 16 == 0, 16 B aligned).

@@ -29,6 +29,8 @@
 //     split softmax.
 // Each page's result is independent of which warp computes it: deterministic.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "akv_common.cuh"
 
@@ -968,6 +970,12 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
   }
 }
 
+}  // namespace akv
+
+#include "akv_qk8.cuh"
+
+namespace akv {
+
 template <int G, bool TRUNC>
 static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
@@ -983,10 +991,23 @@ static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
 
 // G <= 2: the direct-load FHFMA kernel; G >= 4: the tensor-core ring kernel (one
 // K tile feeds 4-8 heads, so the FHFMA path would be issue bound).
+// AKV_QK_KERNEL=tma selects qk8 (the per-warp bulk-copy ring, akv_qk8.cuh) for A/B
+// measurements; the default is the direct-load kernel for G <= 2 and qk5 for G >= 4
+// (measured faster: profiles/r02_qk_tma_vs_ldg.md).
+static bool qk_tma() {
+  static const int v = [] {
+    const char* e = getenv("AKV_QK_KERNEL");
+    return e && strcmp(e, "tma") == 0 ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
-  if constexpr (G >= 4) {
+  if (qk_tma()) {
+    launch_qk8_t<G, TRUNC>(s, cfg, st, max_len, stream);
+  } else if constexpr (G >= 4) {
     launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
   } else {
     const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
