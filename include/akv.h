@@ -71,7 +71,7 @@ typedef struct {
   int32_t n_units;      /* B * Hkv */
   int32_t head_dim;     /* must be AKV_HEAD_DIM */
   int32_t max_pages;    /* page_table row length; capacity = max_pages * P */
-  int32_t reserved;
+  int32_t pool_pages;   /* pages in k_pool / v_pool (0: n_units * max_pages); bounds the TMA tensor maps */
   uint8_t* k_pool;      /* [num_pool_pages][AKV_PAGE_BYTES] */
   uint8_t* v_pool;      /* [num_pool_pages][AKV_PAGE_BYTES] */
   const int32_t* page_table; /* [n_units][max_pages] pool page ids */

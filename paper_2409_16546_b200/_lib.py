@@ -28,7 +28,7 @@ _i32 = ctypes.c_int32
 
 
 class AkvStore(ctypes.Structure):
-    _fields_ = [("n_units", _i32), ("head_dim", _i32), ("max_pages", _i32), ("reserved", _i32),
+    _fields_ = [("n_units", _i32), ("head_dim", _i32), ("max_pages", _i32), ("pool_pages", _i32),
                 ("k_pool", _c), ("v_pool", _c), ("page_table", _c), ("lengths", _c), ("colmax", _c),
                 ("rowmax", _c)]
 

@@ -24,6 +24,10 @@
 // o_partial[h][page]; akv_combine adds o_est and the partials in a fixed order
 // (deterministic).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
 
 #include "akv_common.cuh"
 
@@ -779,10 +783,45 @@ static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   launch_pdl(pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg);
 }
 
+}  // namespace akv
+
+#include "akv_pv4.cuh"
+#include "akv_pv5.cuh"
+
+namespace akv {
+
+// AKV_PV_KERNEL=pv3 / pv4 select the round-1 kernel / the CUDA-core ring kernel for A/B
+// measurements.  Default: pv5 (tensor cores) for the aligned serving step, pv4 for the
+// uniform-tier (forced / baseline) and V-mask export modes.
+static int pv_choice() {
+  static const int v = [] {
+    const char* e = getenv("AKV_PV_KERNEL");
+    if (e && strcmp(e, "pv3") == 0) return 3;
+    if (e && strcmp(e, "pv4") == 0) return 4;
+    return 5;
+  }();
+  return v;
+}
+static bool pv_legacy() { return pv_choice() == 3; }
+
 template <int G>
 static void launch_pv_g(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                         cudaStream_t stream) {
   const bool ex = st.v_tiers != nullptr;
+  if (!pv_legacy()) {
+    if (cfg.trunc_bits) {
+      if (ex) launch_pv4_t<G, true, true, true>(s, cfg, st, max_len, stream);
+      else launch_pv4_t<G, true, false, true>(s, cfg, st, max_len, stream);
+    } else if (cfg.force_tier) {
+      if (ex) launch_pv4_t<G, false, true, true>(s, cfg, st, max_len, stream);
+      else launch_pv4_t<G, false, false, true>(s, cfg, st, max_len, stream);
+    } else if (ex) {
+      launch_pv4_t<G, false, true, false>(s, cfg, st, max_len, stream);
+    } else if (pv_choice() == 4 || !launch_pv5_t<G>(s, cfg, st, max_len, stream)) {
+      launch_pv4_t<G, false, false, false>(s, cfg, st, max_len, stream);
+    }
+    return;
+  }
   if (cfg.trunc_bits) {
     if (ex) launch_pv3_t<G, true, true, true>(s, cfg, st, max_len, stream);
     else launch_pv3_t<G, true, false, true>(s, cfg, st, max_len, stream);
