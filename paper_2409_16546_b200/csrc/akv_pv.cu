@@ -787,18 +787,22 @@ static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
 
 #include "akv_pv4.cuh"
 #include "akv_pv5.cuh"
+#include "akv_pv6.cuh"
 
 namespace akv {
 
-// AKV_PV_KERNEL=pv3 / pv4 select the round-1 kernel / the CUDA-core ring kernel for A/B
-// measurements.  Default: pv5 (tensor cores) for the aligned serving step, pv4 for the
-// uniform-tier (forced / baseline) and V-mask export modes.
+// AKV_PV_KERNEL=pv3 / pv4 / pv5 select the round-1 kernel / the CUDA-core ring kernel /
+// the fixed-slot tensor-core kernel for A/B measurements.  Default: pv6 (variable-size
+// ring, T8 stages on the tensor cores, dense stages through the SIMD element rule) for
+// every aligned mode (serving and V-mask export), pv4 for the uniform-tier (forced /
+// baseline) modes.
 static int pv_choice() {
   static const int v = [] {
     const char* e = getenv("AKV_PV_KERNEL");
     if (e && strcmp(e, "pv3") == 0) return 3;
     if (e && strcmp(e, "pv4") == 0) return 4;
-    return 5;
+    if (e && strcmp(e, "pv5") == 0) return 5;
+    return 6;
   }();
   return v;
 }
@@ -815,6 +819,8 @@ static void launch_pv_g(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
     } else if (cfg.force_tier) {
       if (ex) launch_pv4_t<G, false, true, true>(s, cfg, st, max_len, stream);
       else launch_pv4_t<G, false, false, true>(s, cfg, st, max_len, stream);
+    } else if (pv_choice() == 6 && (ex ? launch_pv6_t<G, true>(s, cfg, st, max_len, stream)
+                                        : launch_pv6_t<G, false>(s, cfg, st, max_len, stream))) {
     } else if (ex) {
       launch_pv4_t<G, false, true, false>(s, cfg, st, max_len, stream);
     } else if (pv_choice() == 4 || !launch_pv5_t<G>(s, cfg, st, max_len, stream)) {
