@@ -46,11 +46,13 @@ struct Pv6Shape {
   static constexpr int HEAD = R * D;              // 4 KB
   // G <= 4: the rule rows accumulate into page-persistent registers (one fold per page);
   // G = 8: passes of 2 q-heads folded per stage (register budget)
-  static constexpr bool PAGEACC = G <= 4;
+  // (G = 4 keeps 12 warps / SM with a 12 KB ring and per-stage folds: measured faster at c3
+  // than 8 warps with page accumulators, 85.9 vs 91.3 us)
+  static constexpr bool PAGEACC = G <= 2;
   static constexpr int HC = PAGEACC ? G : 2;      // q-heads per rule pass
   static constexpr int WARPS = G == 2 ? 5 : 4;
-  static constexpr int MINB = G == 1 ? 3 : 2;     // G = 1: 12 warps / SM, G = 2: 10, G = 4 / 8: 8
-  static constexpr int RING = 16384;              // per-warp stage ring
+  static constexpr int MINB = (G == 1 || G == 4) ? 3 : 2;  // warps / SM: G = 1, 4: 12, G = 2: 10, G = 8: 8
+  static constexpr int RING = G == 4 ? 12288 : 16384;       // per-warp stage ring
   static constexpr int MAXS = RING / HEAD;        // stages in flight at most
   static constexpr int PB = G * R * 4;            // p block [G][R] per stage
   static constexpr int NMETA = 4;                 // page-meta slots
