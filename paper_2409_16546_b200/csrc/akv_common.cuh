@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 
@@ -252,6 +254,56 @@ inline int resident_ctas(int threads, size_t smem) {
   const int r = sms * (per > 0 ? per : 1);
   if (slot) *slot = r;
   return r;
+}
+
+// Host: integer knob from the environment (A/B measurements), read once by the caller.
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// Host: row-major 2-D tensor map (TMA) over a device buffer, cached per (base, shape, box,
+// swizzle) and thread.  The driver entry point is fetched through the runtime (no -lcuda).
+inline bool tmap_2d(void* base, CUtensorMapDataType dt, int esize, unsigned long long inner, unsigned long long outer,
+                    unsigned box_in, unsigned box_out, CUtensorMapSwizzle sw, CUtensorMap* out) {
+  typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (Encode) nullptr;
+    return (Encode)fn;
+  }();
+  if (!encode) return false;
+  struct Entry {
+    void* base;
+    unsigned long long inner, outer;
+    unsigned bi, bo;
+    int sw;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[16];
+  static thread_local int next = 0;
+  for (auto& e : cache)
+    if (e.base == base && e.inner == inner && e.outer == outer && e.bi == box_in && e.bo == box_out && e.sw == (int)sw) {
+      *out = e.map;
+      return true;
+    }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * (unsigned long long)esize};
+  cuuint32_t box[2] = {box_in, box_out};
+  cuuint32_t es[2] = {1, 1};
+  CUtensorMap m;
+  if (encode(&m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[next] = Entry{base, inner, outer, box_in, box_out, (int)sw, m};
+  next = (next + 1) % 16;
+  *out = m;
+  return true;
 }
 
 __device__ __forceinline__ long long status_word(long long code, long long pos) { return (code << 60) | pos; }

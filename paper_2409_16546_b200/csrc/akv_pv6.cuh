@@ -612,45 +612,6 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
   for (int i = 0; i < S::NMETA; ++i) meta_wait(i);
 }
 
-// Row-major 2-D tensor map (no swizzle) over a step buffer, cached per (base, shape, box).
-static bool tmap_rows(void* base, CUtensorMapDataType dt, int esize, unsigned long long inner, unsigned long long outer,
-                      unsigned box_in, unsigned box_out, CUtensorMap* out) {
-  static PFN_encodeTiled encode = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (PFN_encodeTiled) nullptr;
-    return (PFN_encodeTiled)fn;
-  }();
-  if (!encode) return false;
-  struct Entry {
-    void* base;
-    unsigned long long inner, outer;
-    unsigned bi, bo;
-    CUtensorMap map;
-  };
-  static thread_local Entry cache[16];
-  static thread_local int next = 0;
-  for (auto& e : cache)
-    if (e.base == base && e.inner == inner && e.outer == outer && e.bi == box_in && e.bo == box_out) {
-      *out = e.map;
-      return true;
-    }
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * (unsigned long long)esize};
-  cuuint32_t box[2] = {box_in, box_out};
-  cuuint32_t es[2] = {1, 1};
-  CUtensorMap m;
-  if (encode(&m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  cache[next] = Entry{base, inner, outer, box_in, box_out, m};
-  next = (next + 1) % 16;
-  *out = m;
-  return true;
-}
-
 template <int G, bool EXPORT>
 static bool launch_pv6_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
@@ -661,9 +622,9 @@ static bool launch_pv6_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   if (!v_head_tmap(s, &tm)) return false;
   // p [U*G][cap] (box 32 rows x G heads), sel words [U*G][cap/32] (box 8 x G), need words
   // [U*G*2][cap/32] (box 8 x 2G): the G heads of a unit are consecutive rows
-  if (!tmap_rows(st.probs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cap, heads, 32, G, &tp)) return false;
-  if (!tmap_rows(st.sel_bits, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, cap / 32, heads, 8, G, &ts)) return false;
-  if (!tmap_rows(st.need_bits, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, cap / 32, 2 * heads, 8, 2 * G, &tn)) return false;
+  if (!tmap_2d(st.probs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, cap, heads, 32, G, CU_TENSOR_MAP_SWIZZLE_NONE, &tp)) return false;
+  if (!tmap_2d(st.sel_bits, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, cap / 32, heads, 8, G, CU_TENSOR_MAP_SWIZZLE_NONE, &ts)) return false;
+  if (!tmap_2d(st.need_bits, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, cap / 32, 2 * heads, 8, 2 * G, CU_TENSOR_MAP_SWIZZLE_NONE, &tn)) return false;
   const int resident = resident_ctas<pv6_kernel<G, EXPORT>>(32 * S::WARPS, S::SMEM);
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;

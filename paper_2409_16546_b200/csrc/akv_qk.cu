@@ -511,7 +511,7 @@ struct Qk5Shape {
   static constexpr int WARPS = 4;
   static constexpr int NB = 5;  // ring slots per warp
   static constexpr int LIST = (sizeof(Qk5Warp<G>) + 127) & ~127;
-  static constexpr int PER_WARP = LIST + NB * Q5_SLOT;
+  static constexpr int PER_WARP = LIST + NB * Q5_SLOT + 128;  // list | ring | slot mbarriers (TMA staging)
   static constexpr int SMEM = WARPS * PER_WARP;
   static constexpr int MINB = 2;
   static_assert(G * Q5_CHUNKS * 8 * 3 <= NB * Q5_SLOT, "prologue scratch must fit the ring");
@@ -639,6 +639,52 @@ __device__ __forceinline__ void q5_issue(uint8_t* slot, const Qk5Warp<G>& ws, in
   cp_async_commit();
 }
 
+// 2-D TMA gather of four rows (UTMALDG.2D.GATHER4): rows r0..r3 of the map, column 0, into
+// four consecutive rows at dst.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Slot b of a page by TMA gathers (lane 0): the K pool as rows of 256 B (t256: head rows,
+// channel c of page pid = row 256 pid + c) and of 128 B (t128: mid row = 512 pid + 256 + c,
+// low row = 512 pid + 384 + c).  A slot's positions without a low row gather their own mid
+// row again instead (an L2 hit: no extra DRAM bytes; the word is not used).
+template <int G>
+__device__ __forceinline__ void q5_issue_tma(uint8_t* slot, uint64_t* bar, const Qk5Warp<G>& ws, int b, long long pid,
+                                             const CUtensorMap* t256, const CUtensorMap* t128) {
+  const int n8s = ws.n8p >> 4;
+  const int h0 = (int)(pid * 256), m0 = (int)(pid * 512) + 256;
+  if (b < n8s) {
+    const int p0 = 16 * b;
+    mbar_arrive_expect_tx(bar, 4096);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 o = *reinterpret_cast<const uint4*>(&ws.off[p0 + 4 * q]);
+      tma_gather4(slot + q * 1024, t256, h0 + (int)(o.x >> 8), h0 + (int)(o.y >> 8), h0 + (int)(o.z >> 8),
+                  h0 + (int)(o.w >> 8), bar);
+    }
+  } else {
+    const int p0 = ws.n8p + 8 * (b - n8s);
+    const uint32_t lowm = (ws.low[p0 >> 5] >> (p0 & 31)) & 0xFFu;
+    mbar_arrive_expect_tx(bar, 4096);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint4 o = *reinterpret_cast<const uint4*>(&ws.off[p0 + 4 * q]);
+      const int c0 = (int)(o.x >> 8), c1 = (int)(o.y >> 8), c2 = (int)(o.z >> 8), c3 = (int)(o.w >> 8);
+      tma_gather4(slot + q * 1024, t256, h0 + c0, h0 + c1, h0 + c2, h0 + c3, bar);
+      tma_gather4(slot + 2048 + q * 512, t128, m0 + c0, m0 + c1, m0 + c2, m0 + c3, bar);
+      const uint32_t lm = lowm >> (4 * q);
+      tma_gather4(slot + 3072 + q * 512, t128, m0 + c0 + ((lm & 1u) ? 128 : 0), m0 + c1 + ((lm & 2u) ? 128 : 0),
+                  m0 + c2 + ((lm & 4u) ? 128 : 0), m0 + c3 + ((lm & 8u) ? 128 : 0), bar);
+    }
+  }
+}
+
 struct K5Head {
   uint4 h[2][2];  // [channel][page half]: 16 tokens each
 };
@@ -724,7 +770,7 @@ __device__ __forceinline__ void k5_compute_full(const K5Head& X, const K5Nib& N,
   }
 }
 
-template <int G, bool TRUNC>
+template <int G, bool TRUNC, bool TMAQ>
 __device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>& ws, int b, float (&acc)[16][4],
                                            uint32_t tkm, uint32_t tf, uint32_t c80) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -751,7 +797,7 @@ __device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         X.h[j][hf] = *reinterpret_cast<const uint4*>(slot + r * 256 + 128 * hf + 16 * g);
-        const int nb = 2048 + r * 128 + ((64 * hf + 8 * g) ^ ((t & 1) << 6));
+        const int nb = 2048 + r * 128 + (TMAQ ? 64 * hf + 8 * g : ((64 * hf + 8 * g) ^ ((t & 1) << 6)));
         N.m[j][hf] = *reinterpret_cast<const uint2*>(slot + nb);
         N.l[j][hf] = ((lowm >> j) & 1u) ? *reinterpret_cast<const uint2*>(slot + nb + 1024)
                                         : make_uint2(0x88888888u, 0x88888888u);
@@ -806,9 +852,10 @@ __device__ __forceinline__ void k5_finish(const float (&raw)[16], int tok0, int 
   }
 }
 
-template <int G, bool TRUNC>
+template <int G, bool TRUNC, bool TMAQ>
 __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
-    qk5_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, float isd, int npg_max) {
+    qk5_kernel(akv_store_t s, akv_cfg_t cfg, akv_step_t st, int cap, float isd, int npg_max,
+               const __grid_constant__ CUtensorMap t256, const __grid_constant__ CUtensorMap t128) {
   using S = Qk5Shape<G>;
   constexpr int NB = S::NB;
   pdl_trigger();
@@ -818,6 +865,15 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
   const int g = lane >> 2, t = lane & 3;
   Qk5Warp<G>& ws = *reinterpret_cast<Qk5Warp<G>*>(qk5_smem + warp * S::PER_WARP);
   uint8_t* ring = qk5_smem + warp * S::PER_WARP + S::LIST;
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(ring + NB * Q5_SLOT);  // TMAQ: one mbarrier per slot
+  if (TMAQ) {
+    if (lane == 0) {
+      for (int i = 0; i < NB; ++i) mbar_init(&sbar[i], 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+  }
+  uint32_t sphase = 0u;  // TMAQ: parity bit per slot
   uint32_t tkm = 0xFFFFFFFFu, tf = 0u, c80 = 0x80808080u;
   asm volatile("" : "+r"(c80));
   if (TRUNC) {
@@ -866,9 +922,11 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
   int lb = 0, cb = 0, issued = 0, computed = 0, islot = 0, cslot = 0;
   bool lblocked = false;  // the load cursor reached a unit whose lists are not built yet
   const uint8_t* lbase = nullptr;
+  long long lpid = 0;
   if (lc.i < i1) {
     k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, lc.u, lup.n, lc.pg == 0);
-    lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
+    lpid = (long long)unit_page(lup, s, lc.pg);
+    lbase = s.k_pool + lpid * PAGE;
   }
   float acc[16][4];
 #pragma unroll
@@ -880,7 +938,12 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
   auto issue_one = [&]() {
     if (lc.i < i1 && !lblocked) {
       const int nslots = (ws.n8p >> 4) + ((ws.nlp - ws.n8p) >> 3);
-      q5_issue<G>(ring + islot * Q5_SLOT, ws, lb, lbase);
+      if (TMAQ) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads / scratch before async writes
+        if (lane == 0) q5_issue_tma<G>(ring + islot * Q5_SLOT, &sbar[islot], ws, lb, lpid, &t256, &t128);
+      } else {
+        q5_issue<G>(ring + islot * Q5_SLOT, ws, lb, lbase);
+      }
       ++issued;
       islot = islot + 1 == NB ? 0 : islot + 1;
       if (++lb == nslots) {
@@ -888,11 +951,15 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
         const int pu = lc.u;
         advance(lc, lup);
         if (lc.i < i1) {
-          if (lc.u != pu) lblocked = true;  // new unit: wait for the math to drain
-          else lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
+          if (lc.u != pu) {
+            lblocked = true;  // new unit: wait for the math to drain
+          } else {
+            lpid = (long long)unit_page(lup, s, lc.pg);
+            lbase = s.k_pool + lpid * PAGE;
+          }
         }
       }
-    } else {
+    } else if (!TMAQ) {
       cp_async_commit();
     }
   };
@@ -903,15 +970,21 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
     if (issued == computed) {
       // drained at a unit boundary: build the next unit's lists, refill the ring
       k5_prologue<G, TRUNC>(ws, ring, s, cfg, st, lc.u, lup.n, lc.pg == 0);
-      lbase = s.k_pool + unit_page(lup, s, lc.pg) * PAGE;
+      lpid = (long long)unit_page(lup, s, lc.pg);
+      lbase = s.k_pool + lpid * PAGE;
       lblocked = false;
 #pragma unroll 1
       for (int k = 0; k < NB - 1; ++k) issue_one();
       continue;
     }
-    cp_async_wait<NB - 2>();
+    if (TMAQ) {
+      mbar_wait(&sbar[cslot], (sphase >> cslot) & 1u);
+      sphase ^= 1u << cslot;
+    } else {
+      cp_async_wait<NB - 2>();
+    }
     __syncwarp();
-    q5_compute<G, TRUNC>(ring + cslot * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
+    q5_compute<G, TRUNC, TMAQ>(ring + cslot * Q5_SLOT, ws, cb, acc, tkm, tf, c80);
     ++computed;
     cslot = cslot + 1 == NB ? 0 : cslot + 1;
     __syncwarp();  // every lane is done with the slot before it is refilled
@@ -976,17 +1049,36 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
 
 namespace akv {
 
+// AKV_QK5_TMA=1 stages qk5's slots by TMA gathers (four channel rows per
+// UTMALDG.2D.GATHER4, parity-green) instead of 16-byte cp.async: measured slower at c3
+// (qk 144.5 vs 133.1 us, profiles/r02_history.md r2-4), so the default stays cp.async.
 template <int G, bool TRUNC>
 static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
                          cudaStream_t stream) {
   using S = Qk5Shape<G>;
-  const int resident = resident_ctas<qk5_kernel<G, TRUNC>>(32 * S::WARPS, S::SMEM);
+  static const int use_tma = env_int("AKV_QK5_TMA", 0);
+  const unsigned long long pages = s.pool_pages > 0 ? (unsigned long long)s.pool_pages
+                                                    : (unsigned long long)s.n_units * s.max_pages;
+  CUtensorMap t256, t128;
+  const bool tma = use_tma && tmap_2d(s.k_pool, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 256, pages * 256, 256, 1,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE, &t256) &&
+                   tmap_2d(s.k_pool, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 128, pages * 512, 128, 1,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, &t128);
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
   const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  launch_pdl(qk5_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
+  if (tma) {
+    const int resident = resident_ctas<qk5_kernel<G, TRUNC, true>>(32 * S::WARPS, S::SMEM);
+    const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+    launch_pdl(qk5_kernel<G, TRUNC, true>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap,
+               isd, npg, t256, t128);
+    return;
+  }
+  const int resident = resident_ctas<qk5_kernel<G, TRUNC, false>>(32 * S::WARPS, S::SMEM);
+  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  launch_pdl(qk5_kernel<G, TRUNC, false>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd,
+             npg, t256, t128);
 }
 
 // G <= 2: the direct-load FHFMA kernel; G >= 4: the tensor-core ring kernel (one
