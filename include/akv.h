@@ -8,6 +8,7 @@
  * /root/reference).  Each entry point below cites the reference interface it
  * replaces:
  *   akv_append            <- KVStore.append_token
+ *   akv_append_ws         <- KVStore.append (bulk / prefill) SPEC.md:233-241
  *                            (+ split_chunks HB:154-157, ColMax/RowMax SPEC.md:219-226,278-279)
  *   akv_qk                <- attention_decode.scores_aligned SPEC.md:315-323
  *                            (k_channel_tiers/rule1_target SPEC.md:157-183,
@@ -130,6 +131,18 @@ int akv_step_carve(akv_step_t* step, void* workspace, int32_t n_units, int32_t g
  * outcome it reads (KVStore.append does), so errors survive graph replays. */
 int akv_append(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t n_new,
                int64_t* status, void* stream);
+
+/* Bulk append (prefill writer) with a caller workspace of
+ * akv_append_workspace_bytes(n_units, n_new) bytes (no zeroing needed): one CTA per
+ * (unit, page span) stages the span's K rows in shared memory and writes the
+ * channel-major K planes / token-major V planes with 16 B stores, validation fused
+ * in; a per-unit commit rejects the whole append (same status words and stickiness
+ * as akv_append) or folds the ColMax partials and bumps the length.  k, v 16 B
+ * aligned.  n_new == 1 runs akv_append.  Replaces KVStore.append (bulk form,
+ * SPEC.md:233-241). */
+int64_t akv_append_workspace_bytes(int32_t n_units, int32_t n_new);
+int akv_append_ws(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t n_new, int64_t* status,
+                  void* workspace, int64_t workspace_bytes, void* stream);
 
 /* max_len: host-side upper bound on lengths[] (sizes the grid). */
 int akv_qk(const akv_store_t* store, const akv_cfg_t* cfg, const akv_step_t* step, int32_t max_len,

@@ -72,6 +72,10 @@ def lib():
         L.akv_step_carve.argtypes = [P(AkvStep), _c, _i32, _i32, _i32]
         L.akv_append.restype = _i32
         L.akv_append.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c]
+        L.akv_append_workspace_bytes.restype = ctypes.c_int64
+        L.akv_append_workspace_bytes.argtypes = [_i32, _i32]
+        L.akv_append_ws.restype = _i32
+        L.akv_append_ws.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c, ctypes.c_int64, _c]
         for name in ("akv_qk", "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step"):
             f = getattr(L, name)
             f.restype = _i32
@@ -84,7 +88,8 @@ def lib():
         return L
 
 
-EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_qk",
+EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_append_workspace_bytes",
+                    "akv_append_ws", "akv_qk",
                     "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step", "akv_export_planes",
                     "akv_error_histogram")
 

@@ -198,14 +198,29 @@ class KVStore:
         if int(self._host_len.max()) + T > self.capacity:
             raise ValueError(f"append of {T} tokens exceeds capacity {self.capacity}")
         self.status_dev.zero_()  # status words are sticky (akv.h): clear before an append whose outcome we read
-        rc = self._L.akv_append(ctypes.byref(self.c_store), k.data_ptr(), v.data_ptr(), T,
-                                self.status_dev.data_ptr(), self._stream())
+        if T == 1:
+            rc = self._L.akv_append(ctypes.byref(self.c_store), k.data_ptr(), v.data_ptr(), T,
+                                    self.status_dev.data_ptr(), self._stream())
+        else:  # prefill writer: page-span tiles, fused validation, per-unit commit
+            ws = self._append_workspace(T)
+            rc = self._L.akv_append_ws(ctypes.byref(self.c_store), k.data_ptr(), v.data_ptr(), T,
+                                       self.status_dev.data_ptr(), ws.data_ptr(), ws.numel(), self._stream())
         _lib.check(rc, "akv_append")
         before = self._host_len.copy()
         self._host_len += T
         self._pending = (k, v, before, T)
         if self.strict:
             self.check()
+
+    def _append_workspace(self, T: int):
+        """Device workspace of the bulk append (a ColMax row + the earliest non-finite key per unit),
+        grown on demand and reused; the kernels rewrite every byte they read."""
+        need = int(self._L.akv_append_workspace_bytes(self.n_units, T))
+        ws = getattr(self, "_append_ws", None)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._append_ws = ws
+        return ws
 
     def check(self) -> None:
         """Synchronise on the last append's status; raise ValueError with the position."""

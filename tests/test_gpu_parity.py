@@ -427,3 +427,63 @@ def test_decode_graph_errors_are_sticky_and_capacity_guarded():
     assert st.lengths_dev.cpu().tolist() == [256, 255]
     with pytest.raises(ValueError, match="store is full"):
         dg.step(q, kt[:, :, n + 1], vt[:, :, n + 1])
+
+
+@pytest.mark.parametrize("chunks", [(37, 300, 1), (256, 255, 2), (1, 511, 90), (700,)])
+def test_prefill_writer_spans_bitexact(chunks):
+    """akv_append_ws (page-span tiles): successive bulk appends starting mid-page and mid
+    16-token group must leave the planes / sidecars equal to the oracle's (merge path at
+    both span ends), and the old bytes of the page outside each span untouched."""
+    n = sum(chunks)
+    B, Hkv = 1, 3
+    K, V, _ = generate_batch(B, Hkv, n, 128, 1, seed=5 + n)
+    st = KVStore(B, Hkv, 128, 1024)
+    kt = torch.from_numpy(K.view(np.int16)).view(B, Hkv, n, 128)
+    vt = torch.from_numpy(V.view(np.int16)).view(B, Hkv, n, 128)
+    t = 0
+    for c in chunks:
+        st.append(kt[:, :, t:t + c], vt[:, :, t:t + c])
+        t += c
+    st.check()
+    for which, src in (("k", K), ("v", V)):
+        p0, p1, p2 = st.export_planes(which)
+        for u in range(Hkv):
+            ref = OPlane.from_words(src[u])
+            assert np.array_equal(p0[0, u], ref.plane0)
+            assert np.array_equal(p1[0, u], ref.plane1)
+            assert np.array_equal(p2[0, u], ref.plane2)
+    cm = st.colmax().cpu().numpy()
+    rm = st.rowmax().cpu().numpy().view(np.uint16)
+    for u in range(Hkv):
+        from oracle.kv_store import KVStore as OStore
+        o = OStore(128)
+        o.append_rows(K[u], V[u])
+        assert np.array_equal(cm[0, u].astype(np.uint16), o.colmax)
+        assert np.array_equal(rm[0, u, :n], o.rowmax)
+    assert (st.lengths == n).all()
+
+
+def test_prefill_writer_earliest_offender_and_capacity():
+    """The fused validation reports the earliest offending word over all page spans (token,
+    then K before V, then channel), refuses the unit's whole append (length, ColMax
+    unchanged) and commits the other units; an append beyond capacity is refused."""
+    st = KVStore(1, 2, 128, 1024)
+    st.append(torch.randn(1, 2, 100, 128).half(), torch.randn(1, 2, 100, 128).half())
+    cm0 = st.colmax().clone()
+    k = torch.randn(1, 2, 600, 128).half()
+    v = torch.randn(1, 2, 600, 128).half()
+    k[0, 0, 550, 3] = float("inf")   # later span
+    v[0, 0, 400, 100] = float("nan")  # earlier token (V): reported
+    k[0, 0, 400, 120] = float("-inf")  # same token, K before V: reported first
+    k[0, 1, 10] *= 1000  # unit 1 commits (ColMax grows)
+    with pytest.raises(ValueError, match=r"in K at batch 0, kv-head 0, token 500, channel 120"):
+        st.append(k, v)
+    assert st.lengths.tolist() == [[100, 700]]
+    cm = st.colmax()
+    assert torch.equal(cm[0, 0], cm0[0, 0])
+    assert bool((cm[0, 1] >= cm0[0, 1]).all()) and not torch.equal(cm[0, 1], cm0[0, 1])
+    st2 = KVStore(1, 1, 128, 256)
+    st2.append(torch.randn(1, 1, 200, 128).half(), torch.randn(1, 1, 200, 128).half())
+    with pytest.raises(ValueError, match="capacity"):
+        st2.append(torch.randn(1, 1, 100, 128).half(), torch.randn(1, 1, 100, 128).half())
+    assert st2.lengths.tolist() == [[200]]
