@@ -9,6 +9,7 @@
  * replaces:
  *   akv_append            <- KVStore.append_token
  *   akv_append_ws         <- KVStore.append (bulk / prefill) SPEC.md:233-241
+ *   akv_read_elements     <- KVStore.read_element / read_channel SPEC.md:242-259
  *                            (+ split_chunks HB:154-157, ColMax/RowMax SPEC.md:219-226,278-279)
  *   akv_qk                <- attention_decode.scores_aligned SPEC.md:315-323
  *                            (k_channel_tiers/rule1_target SPEC.md:157-183,
@@ -143,6 +144,15 @@ int akv_append(const akv_store_t* store, const uint16_t* k, const uint16_t* v, i
 int64_t akv_append_workspace_bytes(int32_t n_units, int32_t n_new);
 int akv_append_ws(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t n_new, int64_t* status,
                   void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Metered reads: n requests (unit, token, channel, tier code 0/8/12/16) of plane set
+ * which (0 = K, 1 = V); out[i] = the word rebuilt at the tier with the midpoint fill
+ * (SKIP -> 0); counters[3] (int64, device) += elements read at T8 / T12 / T16.  Only the
+ * planes a tier needs are touched.  Out-of-range requests give 0 and are not counted.
+ * Replaces KVStore.read_element / read_channel. */
+int akv_read_elements(const akv_store_t* store, int32_t which, const int32_t* unit, const int32_t* tok,
+                      const int32_t* chan, const int32_t* tier, int64_t n, uint16_t* out, int64_t* counters,
+                      void* stream);
 
 /* max_len: host-side upper bound on lengths[] (sizes the grid). */
 int akv_qk(const akv_store_t* store, const akv_cfg_t* cfg, const akv_step_t* step, int32_t max_len,

@@ -74,6 +74,8 @@ def lib():
         L.akv_append.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c]
         L.akv_append_workspace_bytes.restype = ctypes.c_int64
         L.akv_append_workspace_bytes.argtypes = [_i32, _i32]
+        L.akv_read_elements.restype = _i32
+        L.akv_read_elements.argtypes = [P(AkvStore), _i32, _c, _c, _c, _c, ctypes.c_int64, _c, _c, _c]
         L.akv_append_ws.restype = _i32
         L.akv_append_ws.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c, ctypes.c_int64, _c]
         for name in ("akv_qk", "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step"):
@@ -89,7 +91,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_append_workspace_bytes",
-                    "akv_append_ws", "akv_qk",
+                    "akv_append_ws", "akv_read_elements", "akv_qk",
                     "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step", "akv_export_planes",
                     "akv_error_histogram")
 

@@ -437,9 +437,81 @@ __global__ void __launch_bounds__(D) append_commit_ws_kernel(akv_store_t s, int 
   if (c == 0) s.lengths[u] = t0 + n_new;
 }
 
+// ---------------------------------------------------------------------------
+// Metered reads (KVStore.read_element / read_channel): one thread per
+// request reads only the planes its tier needs (head byte; + mid nibble for T12 / T16;
+// + low nibble for T16), rebuilds the word with the midpoint fill (HB:160-179) and
+// counts the element at its tier (warp-aggregated atomics); SKIP reads nothing and
+// returns 0.  Out-of-range requests return 0 and are not counted.
+// ---------------------------------------------------------------------------
+__global__ void read_elements_kernel(akv_store_t s, int which, const int32_t* __restrict__ unit,
+                                     const int32_t* __restrict__ tok, const int32_t* __restrict__ chan,
+                                     const int32_t* __restrict__ tier, long long n, uint16_t* __restrict__ out,
+                                     unsigned long long* __restrict__ counters) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int code = 0;
+  uint32_t w = 0u;
+  if (i < n) {
+    const int u = unit[i], t = tok[i], c = chan[i];
+    code = tier[i];
+    if (u < 0 || u >= s.n_units || c < 0 || c >= D || t < 0 || t >= s.lengths[u] || code == 0) {
+      code = 0;
+    } else {
+      const uint8_t* pg = (which ? s.v_pool : s.k_pool) +
+                          (size_t)s.page_table[(size_t)u * s.max_pages + t / P] * PAGE;
+      const int tt = t % P;
+      int hb, nb;
+      bool hi;  // mid nibble in the high half of its byte (low nibble in the other half)
+      if (which == 0) {  // K: channel-major, nibble words over 8 tokens
+        hb = c * P + tt;
+        nb = c * (P / 2) + (tt >> 3) * 4 + (tt & 3);
+        hi = (tt & 7) < 4;
+      } else {  // V: token-major, nibble words over 8 channels
+        hb = tt * D + c;
+        nb = tt * (D / 2) + (c >> 3) * 4 + (c & 3);
+        hi = (c & 7) < 4;
+      }
+      w = (uint32_t)pg[hb] << 8;
+      if (code >= 12) {
+        const uint32_t mb = pg[MID + nb];
+        w |= (hi ? (mb >> 4) : (mb & 0xFu)) << 4;
+        if (code >= 16) {
+          const uint32_t lb = pg[LOW + nb];
+          w |= hi ? (lb & 0xFu) : (lb >> 4);
+        } else {
+          w |= 0x8u;
+        }
+      } else {
+        w |= 0x80u;
+      }
+    }
+    out[i] = (uint16_t)w;
+  }
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, code == 8 + 4 * k);
+    if (b && lane == 0) atomicAdd(counters + k, (unsigned long long)__popc(b));
+  }
+}
+
 }  // namespace akv
 
 using namespace akv;
+
+extern "C" int akv_read_elements(const akv_store_t* store, int32_t which, const int32_t* unit, const int32_t* tok,
+                                 const int32_t* chan, const int32_t* tier, int64_t n, uint16_t* out, int64_t* counters,
+                                 void* stream) {
+  if (!store || (which != 0 && which != 1) || n < 0 || (n > 0 && (!unit || !tok || !chan || !tier || !out)) ||
+      !counters)
+    return AKV_EINVAL;
+  if (store->head_dim != D) return AKV_EUNSUPPORTED;
+  if (n == 0) return AKV_OK;
+  const int threads = 256;
+  read_elements_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+      *store, which, unit, tok, chan, tier, n, out, reinterpret_cast<unsigned long long*>(counters));
+  return cudaGetLastError() == cudaSuccess ? AKV_OK : AKV_ECUDA;
+}
 
 extern "C" int64_t akv_append_workspace_bytes(int32_t n_units, int32_t n_new) {
   if (n_units <= 0 || n_new <= 0) return 0;

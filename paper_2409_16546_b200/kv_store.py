@@ -307,38 +307,59 @@ class KVStore:
         return PlaneTensor(self.n_dims, p0, p1, p2).words()
 
     # ---------------------------------------------------------------- metered reads
+    def read_elements(self, units, toks, chans, tiers, which: str = "k", counter: AccessCounter = None) -> torch.Tensor:
+        """Batched metered reads on the device (akv_read_elements): int32 tensors / sequences of
+        equal length; returns the rebuilt words [n] (uint16 patterns as int16).  Only the planes
+        each tier needs are read; the T8 / T12 / T16 element counts go into `counter`."""
+        dev = self.device
+        cols = [torch.as_tensor(x, dtype=torch.int32).reshape(-1).to(dev) for x in (units, toks, chans, tiers)]
+        n = int(cols[0].numel())
+        if any(int(x.numel()) != n for x in cols):
+            raise ValueError("read_elements: argument lengths differ")
+        out = torch.empty(n, dtype=torch.int16, device=dev)
+        cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+        rc = self._L.akv_read_elements(ctypes.byref(self.c_store), {"k": 0, "v": 1}[which], cols[0].data_ptr(),
+                                       cols[1].data_ptr(), cols[2].data_ptr(), cols[3].data_ptr(), n, out.data_ptr(),
+                                       cnt.data_ptr(), self._stream())
+        _lib.check(rc, "akv_read_elements")
+        if counter is not None:
+            c8, c12, c16 = (int(x) for x in cnt.cpu())
+            counter.t8 += c8
+            counter.t12 += c12
+            counter.t16 += c16
+        return out
+
+    @staticmethod
+    def _tier_code(tier) -> int:
+        code = int(tier)
+        if code not in (0, 8, 12, 16):
+            raise ValueError(f"bad tier {tier}")
+        return code
+
     def read_element(self, b: int, h: int, t: int, c: int, tier, counter: AccessCounter, which: str = "k") -> int:
-        """Host-side metered read of one element (API parity; not a hot path)."""
+        """KVStore.read_element: one metered read on the device; SKIP -> 0, 0 bits."""
         n = int(self._host_len[b * self.n_kv_heads + h])
         if not (0 <= t < n and 0 <= c < self.n_dims):
             raise IndexError("read out of range")
-        tier = int(tier)
-        if tier == 0:
+        code = self._tier_code(tier)
+        if code == 0:
             return 0
-        w = int(self.words(which)[b, h, t, c])
-        if tier == 8:
-            counter.t8 += 1
-            return (w & 0xFF00) | 0x80
-        if tier == 12:
-            counter.t12 += 1
-            return (w & 0xFFF0) | 0x8
-        if tier == 16:
-            counter.t16 += 1
-            return w
-        raise ValueError(f"bad tier {tier}")
+        w = self.read_elements([b * self.n_kv_heads + h], [t], [c], [code], which, counter)
+        return int(w.item()) & 0xFFFF
 
     def read_channel(self, b: int, h: int, c: int, tier, counter: AccessCounter, which: str = "k") -> np.ndarray:
+        """KVStore.read_channel: tokens 0..n-1 of channel c at one tier."""
+        if not 0 <= c < self.n_dims:
+            raise IndexError("read out of range")
         n = int(self._host_len[b * self.n_kv_heads + h])
-        tier = int(tier)
-        col = self.words(which)[b, h, :n, c]
-        if tier == 0:
+        code = self._tier_code(tier)
+        if code == 0:
             return np.zeros(n, np.uint16)
-        setattr(counter, f"t{tier}", getattr(counter, f"t{tier}") + n)
-        if tier == 8:
-            return ((col & 0xFF00) | 0x80).astype(np.uint16)
-        if tier == 12:
-            return ((col & 0xFFF0) | 0x8).astype(np.uint16)
-        return col.astype(np.uint16)
+        u = b * self.n_kv_heads + h
+        w = self.read_elements(torch.full((n,), u, dtype=torch.int32), torch.arange(n, dtype=torch.int32),
+                               torch.full((n,), c, dtype=torch.int32), torch.full((n,), code, dtype=torch.int32),
+                               which, counter)
+        return w.cpu().numpy().view(np.uint16)
 
     # ---------------------------------------------------------------- decode workspaces
     def workspace(self, group: int, separate_probs: bool = False):

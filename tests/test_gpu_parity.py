@@ -487,3 +487,39 @@ def test_prefill_writer_earliest_offender_and_capacity():
     with pytest.raises(ValueError, match="capacity"):
         st2.append(torch.randn(1, 1, 100, 128).half(), torch.randn(1, 1, 100, 128).half())
     assert st2.lengths.tolist() == [[200]]
+
+
+def test_metered_reads_match_oracle():
+    """KVStore.read_element / read_channel / read_elements on the device (akv_read_elements)
+    against the oracle's metered reads: rebuilt words bit-exact at every
+    tier (SKIP -> 0, 0 bits), AccessCounter totals equal, K and V, pages crossed."""
+    from oracle.kv_store import AccessCounter as OCounter
+    from paper_2409_16546_b200 import AccessCounter
+    c = Case(B=2, Hkv=2, n=600, seed=77)
+    rng = np.random.default_rng(3)
+    for which in ("k", "v"):
+        units = rng.integers(0, 4, 500)
+        toks = rng.integers(0, 600, 500)
+        chans = rng.integers(0, 128, 500)
+        tiers = rng.choice([0, 8, 12, 16], 500)
+        gc = AccessCounter()
+        got = c.store.read_elements(units, toks, chans, tiers, which, gc).cpu().numpy().view(np.uint16)
+        oc = OCounter()
+        for i in range(500):
+            o = c.ostore(int(units[i]))
+            plane = o.k if which == "k" else o.v
+            ref = o.read_element(plane, int(toks[i]), int(chans[i]), int(tiers[i]), oc)
+            assert int(got[i]) == int(ref) & 0xFFFF, (which, i)
+        assert (gc.t8, gc.t12, gc.t16) == (oc.t8, oc.t12, oc.t16)
+        for tier in (0, 8, 12, 16):
+            gc, oc = AccessCounter(), OCounter()
+            col = c.store.read_channel(1, 0, 77, tier, gc, which)
+            o = c.ostore(2)
+            ref = o.read_channel(o.k if which == "k" else o.v, 77, tier, oc)
+            assert np.array_equal(col, np.asarray(ref, dtype=np.uint16))
+            assert gc.bits_read == oc.bits_read
+        gc = AccessCounter()
+        assert c.store.read_element(0, 1, 599, 127, 12, gc, which) == \
+            c.ostore(1).read_element(c.ostore(1).k if which == "k" else c.ostore(1).v, 599, 127, 12, OCounter())
+    with pytest.raises(IndexError):
+        c.store.read_element(0, 0, 600, 0, 8, AccessCounter())
