@@ -66,6 +66,9 @@ struct Pv6Shape {
   static constexpr int OFF_SCR = OFF_G1 + G * 256;
   static constexpr int OFF_NE = OFF_SCR + SCR;            // [G][R] packed -ep words of the stage's rows
   static constexpr int OFF_BAR = OFF_NE + G * R * 4;
+  static constexpr int DENSE_MIN = 20;
+  static constexpr bool USE_DENSE = G <= 2;               // G >= 4: registers (the SPARSE path takes every plan row)
+  static constexpr int RULE_UNROLL = G >= 2 ? 1 : 2;     // rule-loop unroll (register budget)                    // plan rows from which a full stage goes DENSE
   static constexpr int MISC = (OFF_BAR + (MAXS + NMETA) * 8 + 127) & ~127;
   static constexpr int SMEM = WARPS * (RING + MISC) + 1024;  // + 1 KB alignment slack
 };
@@ -92,17 +95,25 @@ __device__ __forceinline__ void pv6_copy_runs(uint32_t m, uint8_t* dst0, const u
   }
 }
 
-// Rule-path partials of HC q-heads (heads p0 ..): element counts into adj (the packed
-// counters count down: a mask half is -1), the two row halves folded, and the sums added
-// into the mma accumulators (their channel layout) through shared memory.
+// Decode a packed element count accumulated by 32-bit adds of 0xFFFF / 0 half masks:
+// S = 2^16 (B - A) - B (mod 2^32) for A high-half and B low-half hits (each < 2^15).
+__device__ __forceinline__ int pv6_mask_count(uint32_t S) {
+  const uint32_t b = (0u - S) & 0xFFFFu;
+  const int d = (int)(S + b) >> 16;  // B - A
+  return 2 * (int)b - d;
+}
+
+// Rule-path partials of HC q-heads (heads p0 ..): element counts into adj, the two row
+// halves folded, and the sums added into the mma accumulators (their channel layout)
+// through shared memory.
 template <int G, int HC, int NT>
 __device__ __forceinline__ void pv6_fold(float2 (&ad)[HC][4], const uint32_t (&cmk)[HC], const uint32_t (&clk)[HC],
                                          int p0, float* scr, float (&acc)[NT][8][4], int (&adj)[G][3]) {
   const int lane = threadIdx.x & 31, half = lane >> 4, cg = lane & 15, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int jj = 0; jj < HC; ++jj) {
-    const int cm = -((int)(int16_t)(cmk[jj] & 0xFFFFu) + (int)(int16_t)(cmk[jj] >> 16));
-    const int cl = -((int)(int16_t)(clk[jj] & 0xFFFFu) + (int)(int16_t)(clk[jj] >> 16));
+    const int cm = pv6_mask_count(cmk[jj]);
+    const int cl = pv6_mask_count(clk[jj]);
     adj[p0 + jj][0] -= cm;
     adj[p0 + jj][1] += cm - cl;
     adj[p0 + jj][2] += cl;
@@ -143,7 +154,7 @@ struct Pv6Rule {
   const uint8_t* hd;       // the stage: head rows (swizzled) | mid rows | low rows
   const float* pb;         // p block [G][R]
   uint32_t* neb;           // [G][R] packed -ep words
-  const uint32_t* g1s;     // [G][64] packed G1 words of the unit
+  const uint32_t* g1s;     // [G][64] packed G1 + 8 words of the unit
   float* scr;              // fold scratch [HC][D]
   uint8_t* vt;             // V-mask export base of head 0, row r0 (EXPORT), else null
   size_t vt_head;          // export stride between heads (cap * D)
@@ -153,31 +164,41 @@ struct Pv6Rule {
 };
 
 // The per-element rule (ROWS = false, D4, SPEC.md:169 for unknown targets, D5) or the row
-// tier (ROWS = true, D7) on the rows in c.rm; contributions folded into the mma
-// accumulators, element counts into adj.  Rows are split between the two half-warps by
-// the parity of their rank in c.rm (lane = (half, 8 channels)).
-template <int G, bool EXPORT, bool ROWS, bool FULL, int NT>
+// tier (ROWS = true, D7); contributions folded into the mma accumulators, element counts
+// into adj.  SPARSE (DENSE = false): the rows of c.rm, split between the two half-warps by
+// the parity of their rank.  DENSE: all 32 rows of a full stage, row 2 it + half (no
+// per-row branches): rows outside a head's plan and selected rows go through the rule with
+// a threshold that never keeps (selected rows with p = 0: their T16 term is o_est, D6).
+// lane = (half, 8 channels).  With e = max(bexp, 1) and X = G1 - ep (G1 = 18 + target -
+// margin): keep mid <=> e >= clamp(X, 0, 31), keep low <=> e >= clamp(X + 4, 0, 31); both
+// compares share one threshold T = clamp(X + 8, 0, 63): mid <=> e + 8 >= T, low <=> e + 4
+// >= T (HSET2 on the small integers as fp16 patterns).  Element counts: the masks summed
+// by 32-bit adds (pv6_mask_count).
+template <int G, bool EXPORT, bool ROWS, bool DENSE, int NT>
 __device__ __forceinline__ void pv6_rule_rows(const Pv6Rule<G>& c, float (&acc)[NT][8][4], int (&adj)[G][3],
                                               float2 (&pad)[Pv6Shape<G>::HC][4], uint32_t (&pcm)[Pv6Shape<G>::HC],
                                               uint32_t (&pcl)[Pv6Shape<G>::HC]) {
   using S = Pv6Shape<G>;
   constexpr int R = S::R, HC = S::HC;
-  const int lane = threadIdx.x & 31, half = lane >> 4, cg = lane & 15, g = lane >> 2, t = lane & 3;
+  const int lane = threadIdx.x & 31, half = lane >> 4, cg = lane & 15;
   const uint32_t even = __ballot_sync(0xFFFFFFFFu, ((c.rm >> lane) & 1u) && !(__popc(c.rm & ((1u << lane) - 1u)) & 1));
   const uint32_t mine0 = half ? (c.rm & ~even) : even;
-  if (!ROWS) {
-    // lane = row: -ep = -floor(log2 p) for rows in the head's plan with p > 0, else 16000 (never kept
-    // unless the target is unknown)
+  if (!ROWS || DENSE) {
+    // lane = row: -ep = -floor(log2 p) for rows in the head's plan with p > 0; 16000 (kept only
+    // for an unknown target) otherwise; 20000 (never) for selected rows (DENSE)
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const float p = c.pb[j * R + lane];
-      const int ne = (((c.nmw[j] >> lane) & 1u) && p > 0.f) ? -floor_log2f(p) : 16000;
+      const bool sel = (c.selw[j] >> lane) & 1u;
+      int ne = (((c.nmw[j] >> lane) & 1u) && p > 0.f) ? -floor_log2f(p) : 16000;
+      if (DENSE && sel) ne = 20000;
       c.neb[j * R + lane] = (uint32_t)ne * 0x00010001u;
     }
     __syncwarp();
   }
   const uint8_t* nibm = c.hd + S::HEAD;
   const uint8_t* nibl = c.hd + S::HEAD + 64 * c.nm;
+  const uint32_t c8 = 0x00800080u, c12 = 0x00080008u;
 #pragma unroll
   for (int p0 = 0; p0 < G; p0 += HC) {
     float2 adl[HC][4];
@@ -203,55 +224,53 @@ __device__ __forceinline__ void pv6_rule_rows(const Pv6Rule<G>& c, float (&acc)[
     }
     uint32_t mine = mine0;
     int it = 0;
-#pragma unroll 2
-    for (; FULL ? it < 16 : mine != 0u; ++it) {
-      // FULL: all 32 rows valid and in both plans (dense stage): row 2it + half, no ranks
-      const int rr = FULL ? 2 * it + half : __ffs(mine) - 1;
-      if (!FULL) mine &= mine - 1u;
-      const uint32_t bit = 1u << rr;
+#pragma unroll(S::RULE_UNROLL)
+    for (; DENSE ? it < 16 : mine != 0u; ++it) {
+      const int rr = DENSE ? 2 * it + half : __ffs(mine) - 1;
+      if (!DENSE) mine &= mine - 1u;
+      const uint32_t bit = 1u << rr, below = bit - 1u;
       const uint2 hv = *reinterpret_cast<const uint2*>(c.hd + rr * D + (((cg >> 1) ^ (rr & 7)) << 4) + (cg & 1) * 8);
       uint32_t mw = 0u, lw = 0u;
-      if (FULL) {
-        mw = *reinterpret_cast<const uint32_t*>(nibm + 64 * rr + 4 * cg);
-        lw = *reinterpret_cast<const uint32_t*>(nibl + 64 * rr + 4 * cg);
-      } else {
-        if (c.um & bit) mw = *reinterpret_cast<const uint32_t*>(nibm + 64 * __popc(c.um & (bit - 1u)) + 4 * cg);
-        if (c.ul & bit) lw = *reinterpret_cast<const uint32_t*>(nibl + 64 * __popc(c.ul & (bit - 1u)) + 4 * cg);
-      }
-      uint32_t w[4], e2[4], w8[4], w12[4];
+      if (c.um & bit) mw = *reinterpret_cast<const uint32_t*>(nibm + 64 * __popc(c.um & below) + 4 * cg);
+      if (c.ul & bit) lw = *reinterpret_cast<const uint32_t*>(nibl + 64 * __popc(c.ul & below) + 4 * cg);
+      uint32_t w[4], e8[4], e4[4], w8[4], w12[4];
       assemble8(hv.x, hv.y, mw, lw, w);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (!ROWS) {
-          const uint32_t a = __vmaxu2(w[k] & 0x7FFF7FFFu, 0x04000400u);
-          e2[k] = (a >> 10) & 0x001F001Fu;
+          // max(bexp, 1) + 8 and + 4 per half (for HC >= 2 the + 4 is formed per use: registers)
+          e8[k] = __viaddmax_u16x2((w[k] & 0x7C007C00u) >> 10, 0x00080008u, 0x00090009u);
+          if (HC == 1) e4[k] = e8[k] - 0x00040004u;
         }
-        w8[k] = (w[k] & 0xFF00FF00u) | 0x00800080u;
-        w12[k] = (w[k] & 0xFFF0FFF0u) | 0x00080008u;
+        w8[k] = (w[k] & 0xFF00FF00u) | c8;
+        w12[k] = (w[k] & 0xFFF0FFF0u) | c12;
       }
 #pragma unroll
       for (int jj = 0; jj < HC; ++jj) {
         const int j = p0 + jj;
         uint8_t* vt = EXPORT && c.vt ? c.vt + (size_t)j * c.vt_head + (size_t)rr * D + cg * 8 : nullptr;
-        if (c.selw[j] & bit) {  // selected (D6): its T16 term is o_est
+        if ((!DENSE || EXPORT) && (c.selw[j] & bit)) {  // selected (D6): its T16 term is o_est
           if (EXPORT && vt) *reinterpret_cast<uint2*>(vt) = make_uint2(0x10101010u, 0x10101010u);
           continue;
         }
-        const float p = c.pb[j * R + rr];
+        const float p = DENSE && ((c.selw[j] >> rr) & 1u) ? 0.f : c.pb[j * R + rr];
         uint32_t mm[4], ml[4];
         if (ROWS) {
-          const uint32_t a = (c.nmw[j] & bit) ? 0xFFFFFFFFu : 0u, b = (c.nlw[j] & bit) ? 0xFFFFFFFFu : 0u;
+          const bool row_ok = !DENSE || !((c.selw[j] >> rr) & 1u);
+          const uint32_t a = row_ok && (c.nmw[j] & bit) ? 0xFFFFFFFFu : 0u;
+          const uint32_t b = row_ok && (c.nlw[j] & bit) ? 0xFFFFFFFFu : 0u;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             mm[k] = a;
             ml[k] = b;
           }
         } else {
-          const uint32_t nE = c.neb[j * R + rr], nE4 = nE + 0x00040004u;
+          const uint32_t nE = c.neb[j * R + rr];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            mm[k] = hset2_ge(e2[k], __viaddmin_s16x2_relu(g1[jj][k], nE, 0x001F001Fu));
-            ml[k] = hset2_ge(e2[k], __viaddmin_s16x2_relu(g1[jj][k], nE4, 0x001F001Fu));
+            const uint32_t T = __viaddmin_s16x2_relu(g1[jj][k], nE, 0x003F003Fu);
+            mm[k] = hset2_ge(e8[k], T);
+            ml[k] = hset2_ge(HC == 1 ? e4[k] : e8[k] - 0x00040004u, T);
           }
         }
         uint32_t cds[2] = {0u, 0u};
@@ -259,13 +278,13 @@ __device__ __forceinline__ void pv6_rule_rows(const Pv6Rule<G>& c, float (&acc)[
         for (int k = 0; k < 4; ++k) {
           const uint32_t wj = bsel(mm[k], bsel(ml[k], w[k], w12[k]), w8[k]);
           ad[jj][k] = ffma2_scalar(half2_bits_to_float2(wj), p, ad[jj][k]);
-          cmk[jj] = __viaddmin_s16x2(cmk[jj], mm[k], 0x7FFF7FFFu);
-          clk[jj] = __viaddmin_s16x2(clk[jj], ml[k], 0x7FFF7FFFu);
           if (EXPORT) {
             const uint32_t c2 = 0x00080008u + (mm[k] & 0x00040004u) + (ml[k] & 0x00040004u);  // codes 8/12/16
             cds[k >> 1] |= ((c2 & 0xFFu) | ((c2 >> 8) & 0xFF00u)) << (16 * (k & 1));
           }
         }
+        cmk[jj] += (mm[0] + mm[1]) + (mm[2] + mm[3]);
+        clk[jj] += (ml[0] + ml[1]) + (ml[2] + ml[3]);
         if (EXPORT && vt) *reinterpret_cast<uint2*>(vt) = make_uint2(cds[0], cds[1]);
       }
     }
@@ -480,16 +499,18 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
 
     // rows through the CUDA-core rule: the plan rows, or every row when the whole stage is in
     // the plan or the V masks are exported; the tensor cores take the rest at T8
-    const uint32_t rm = (EXPORT || um == vmask) ? vmask : um;
+    // (DENSE: a full stage with most rows in the plan goes through the rule whole)
+    const bool dense = S::USE_DENSE && cfg.strategy != 1 && vmask == 0xFFFFFFFFu && (EXPORT || __popc(um) >= S::DENSE_MIN);
+    const uint32_t rm = (EXPORT || dense || um == vmask) ? vmask : um;
     if (rm) {
       if (cfg.strategy != 1 && g1_unit != cc.u) {
-        // per-unit thresholds G1_c = 18 + target_c - margin (unknown: -16384), channel pairs
+        // per-unit thresholds G1_c + 8 = 26 + target_c - margin (unknown: -16384), channel pairs
         __syncwarp();
         for (int idx = lane; idx < G * 64; idx += 32) {
           const int j = idx >> 6, pr = idx & 63;
           const int2 tg = *reinterpret_cast<const int2*>(st.targets + ((size_t)cc.u * G + j) * D + 2 * pr);
-          const int a = tg.x == AKV_TARGET_UNKNOWN ? -16384 : min(max(18 + tg.x - cfg.margin_bits, -16000), 1000);
-          const int b = tg.y == AKV_TARGET_UNKNOWN ? -16384 : min(max(18 + tg.y - cfg.margin_bits, -16000), 1000);
+          const int a = tg.x == AKV_TARGET_UNKNOWN ? -16384 : min(max(18 + tg.x - cfg.margin_bits, -16000), 1000) + 8;
+          const int b = tg.y == AKV_TARGET_UNKNOWN ? -16384 : min(max(18 + tg.y - cfg.margin_bits, -16000), 1000) + 8;
           g1s[idx] = ((uint32_t)a & 0xFFFFu) | ((uint32_t)b << 16);
         }
         __syncwarp();
@@ -513,9 +534,8 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
         rc.nmw[j] = nmw[j];
         rc.nlw[j] = nlw[j];
       }
-      const bool full = rm == 0xFFFFFFFFu && um == rm && ul == rm;
       if (cfg.strategy == 1) pv6_rule_rows<G, EXPORT, true, false>(rc, acc, adj, pad, pcm, pcl);
-      else if (full) pv6_rule_rows<G, EXPORT, false, true>(rc, acc, adj, pad, pcm, pcl);
+      else if (S::USE_DENSE && dense) pv6_rule_rows<G, EXPORT, false, S::USE_DENSE>(rc, acc, adj, pad, pcm, pcl);
       else pv6_rule_rows<G, EXPORT, false, false>(rc, acc, adj, pad, pcm, pcl);
       pany = true;
     }

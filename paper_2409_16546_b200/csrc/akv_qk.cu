@@ -1046,6 +1046,7 @@ __global__ void __launch_bounds__(32 * Qk5Shape<G>::WARPS, Qk5Shape<G>::MINB)
 }  // namespace akv
 
 #include "akv_qk8.cuh"
+#include "akv_qk9.cuh"
 
 namespace akv {
 
@@ -1081,18 +1082,22 @@ static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
              npg, t256, t128);
 }
 
-// G <= 2: the direct-load FHFMA kernel; G >= 4: the tensor-core ring kernel (one
-// K tile feeds 4-8 heads, so the FHFMA path would be issue bound).
+// G <= 2: the direct-load FHFMA kernel; G >= 4: the mma.sync ring kernel qk5 (one K tile
+// feeds 4-8 heads, so the FHFMA path would be issue bound).  AKV_QK_KERNEL=qk9 selects the
+// tcgen05 / TMEM kernel (parity-green, slower at c3: profiles/r02_history.md r2-7).
 // AKV_QK_KERNEL=tma selects qk8 (the per-warp bulk-copy ring, akv_qk8.cuh) for A/B
 // measurements; the default is the direct-load kernel for G <= 2 and qk5 for G >= 4
 // (measured faster: profiles/r02_qk_tma_vs_ldg.md).
-static bool qk_tma() {
+static int qk_choice() {
   static const int v = [] {
     const char* e = getenv("AKV_QK_KERNEL");
-    return e && strcmp(e, "tma") == 0 ? 1 : 0;
+    if (e && strcmp(e, "tma") == 0) return 8;
+    if (e && strcmp(e, "qk9") == 0) return 9;
+    return 0;
   }();
-  return v != 0;
+  return v;
 }
+static bool qk_tma() { return qk_choice() == 8; }
 
 template <int G, bool TRUNC>
 static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, int max_len,
@@ -1100,7 +1105,8 @@ static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
   if (qk_tma()) {
     launch_qk8_t<G, TRUNC>(s, cfg, st, max_len, stream);
   } else if constexpr (G >= 4) {
-    launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
+    if (qk_choice() == 9) launch_qk9_t<G, TRUNC>(s, cfg, st, max_len, stream);
+    else launch_qk5_t<G, TRUNC>(s, cfg, st, max_len, stream);
   } else {
     const size_t smem = sizeof(QkWarp<G>) * QK_WARPS;
     const int resident = resident_ctas<qk_kernel<G, TRUNC>>(32 * QK_WARPS, smem);
