@@ -352,9 +352,10 @@ class Rig:
         self.ctypes = ctypes
 
     def append(self):
-        self.store.lengths_dev.fill_(self.n - 1)  # every step attends over exactly n tokens
-        self._lib.check(self.L.akv_append(self.cst, self.k_new.data_ptr(), self.v_new.data_ptr(), 1,
-                                          self.store.status_dev.data_ptr(), self.sp), "akv_append")
+        # the new token goes to position n-1 of every unit (akv_append_at: truncate + append in
+        # one launch), so every step attends over exactly n tokens
+        self._lib.check(self.L.akv_append_at(self.cst, self.k_new.data_ptr(), self.v_new.data_ptr(), self.n - 1,
+                                             self.store.status_dev.data_ptr(), self.sp), "akv_append_at")
 
     def step(self, cfg_c, ev=None):
         by = self.ctypes.byref

@@ -58,6 +58,7 @@ enum {
 #define AKV_STATUS_DEGENERATE 2LL /* degenerate dot product (no q_c!=0 with colmax_c!=0) */
 #define AKV_STATUS_BAD_Q 3LL      /* non-finite q; [40..47]=channel */
 #define AKV_STATUS_CAPACITY 4LL   /* append beyond the page table capacity */
+#define AKV_STATUS_POSITION 5LL   /* akv_append_at position beyond the unit's length */
 
 #define AKV_TARGET_UNKNOWN ((int32_t)0x80000000) /* rule2 target for o_est_r == 0 */
 
@@ -132,6 +133,16 @@ int akv_step_carve(akv_step_t* step, void* workspace, int32_t n_units, int32_t g
  * outcome it reads (KVStore.append does), so errors survive graph replays. */
 int akv_append(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t n_new,
                int64_t* status, void* stream);
+
+/* Truncate every unit to pos tokens (pos <= its length, else AKV_STATUS_POSITION and the
+ * unit is unchanged) and append one token there (length = pos + 1): a rollback of
+ * speculative tokens, or a fixed-context replay (benchmarks, DecodeGraph(rewind_to)) in one
+ * launch.  ColMax keeps the running max over every token ever appended (SPEC.md:219-222 is
+ * a running max; withdrawing a truncated token's contribution is not possible), so K tiers
+ * stay sound.  Same validation and sticky status words as akv_append.  Extension: the
+ * reference has no truncation. */
+int akv_append_at(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t pos, int64_t* status,
+                  void* stream);
 
 /* Bulk append (prefill writer) with a caller workspace of
  * akv_append_workspace_bytes(n_units, n_new) bytes (no zeroing needed): one CTA per

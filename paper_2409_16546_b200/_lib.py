@@ -21,7 +21,7 @@ MAX_KSEL = 64
 TARGET_UNKNOWN = -(1 << 31)
 
 AKV_OK, AKV_EINVAL, AKV_EUNSUPPORTED, AKV_ECUDA = 0, -1, -2, -3
-STATUS_NONFINITE, STATUS_DEGENERATE, STATUS_BAD_Q, STATUS_CAPACITY = 1, 2, 3, 4
+STATUS_NONFINITE, STATUS_DEGENERATE, STATUS_BAD_Q, STATUS_CAPACITY, STATUS_POSITION = 1, 2, 3, 4, 5
 
 _c = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -72,6 +72,8 @@ def lib():
         L.akv_step_carve.argtypes = [P(AkvStep), _c, _i32, _i32, _i32]
         L.akv_append.restype = _i32
         L.akv_append.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c]
+        L.akv_append_at.restype = _i32
+        L.akv_append_at.argtypes = [P(AkvStore), _c, _c, _i32, _c, _c]
         L.akv_append_workspace_bytes.restype = ctypes.c_int64
         L.akv_append_workspace_bytes.argtypes = [_i32, _i32]
         L.akv_read_elements.restype = _i32
@@ -90,7 +92,8 @@ def lib():
         return L
 
 
-EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_append_workspace_bytes",
+EXPORTED_SYMBOLS = ("akv_version", "akv_workspace_bytes", "akv_step_carve", "akv_append", "akv_append_at",
+                    "akv_append_workspace_bytes",
                     "akv_append_ws", "akv_read_elements", "akv_qk",
                     "akv_softmax_select", "akv_pv", "akv_combine", "akv_decode_step", "akv_export_planes",
                     "akv_error_histogram")

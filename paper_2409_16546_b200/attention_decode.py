@@ -417,8 +417,9 @@ class DecodeGraph:
     Each replay appends one token per unit (the host length mirror advances)
     and returns o [B, Hq, d] fp32 on the host.  Data-dependent errors stay on
     device: call `check()` to raise them (non-finite K/V, degenerate q).
-    `rewind_to` (benchmarks only) captures a reset of every unit's length
-    before the append, so every replay attends over the same n tokens.  The
+    `rewind_to` (benchmarks, speculative rollback) appends every replay's token
+    at position rewind_to (akv_append_at: truncate + append in one launch), so
+    every replay attends over the same rewind_to + 1 tokens.  The
     grid is sized for the store's capacity (fixed at capture).
     """
 
@@ -469,11 +470,13 @@ class DecodeGraph:
         st = self.store
         if not self.zero_copy_in:
             self.dev_in.copy_(self.host_in, non_blocking=True)
-        if self.rewind_to is not None:
-            st.lengths_dev.fill_(self.rewind_to)
         kk, vv = (self.host_k, self.host_v) if self.zero_copy_in else (self.k, self.v)
-        _lib.check(self._L.akv_append(ctypes.byref(st.c_store), kk.data_ptr(), vv.data_ptr(), 1,
-                                      st.status_dev.data_ptr(), stream_ptr), "akv_append")
+        if self.rewind_to is not None:  # truncate to rewind_to tokens and append, one launch
+            _lib.check(self._L.akv_append_at(ctypes.byref(st.c_store), kk.data_ptr(), vv.data_ptr(), self.rewind_to,
+                                             st.status_dev.data_ptr(), stream_ptr), "akv_append_at")
+        else:
+            _lib.check(self._L.akv_append(ctypes.byref(st.c_store), kk.data_ptr(), vv.data_ptr(), 1,
+                                          st.status_dev.data_ptr(), stream_ptr), "akv_append")
         _lib.check(self._L.akv_decode_step(ctypes.byref(st.c_store), ctypes.byref(self.cfg_c),
                                            ctypes.byref(self.step_c), st.capacity, stream_ptr), "akv_decode_step")
         if not self.zero_copy_out:
@@ -533,6 +536,7 @@ class DecodeGraph:
             code, isv, c, t = decode_status(int(s[bad[0]]))
             b, h = divmod(int(bad[0]), st.n_kv_heads)
             what = {_lib.STATUS_NONFINITE: f"non-finite {'V' if isv else 'K'} channel {c}",
-                    _lib.STATUS_CAPACITY: "capacity exceeded"}.get(code, f"status code {code}")
+                    _lib.STATUS_CAPACITY: "capacity exceeded",
+                    _lib.STATUS_POSITION: "rewind position beyond the stored length"}.get(code, f"status code {code}")
             raise ValueError(f"append failed ({what}) at batch {b}, kv-head {h}")
         _raise_status(self.ws, st)

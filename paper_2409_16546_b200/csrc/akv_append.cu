@@ -8,8 +8,10 @@ namespace akv {
 // ---------------------------------------------------------------------------
 // single-token append: one CTA per unit, thread = channel.
 // ---------------------------------------------------------------------------
+// pos < 0: append at the unit's length; else truncate the unit to pos tokens (pos <= its
+// length) and append there (akv_append_at).
 __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const uint16_t* __restrict__ k,
-                                                         const uint16_t* __restrict__ v, int64_t* status) {
+                                                         const uint16_t* __restrict__ v, int64_t* status, int pos) {
   pdl_trigger();
   pdl_wait();
   const int u = blockIdx.x;
@@ -17,7 +19,8 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   // independent loads first (k, v, length), then the page id: two dependent round trips in all
   const uint32_t kw = k[(size_t)u * D + c];
   const uint32_t vw = v[(size_t)u * D + c];
-  const int t = s.lengths[u];
+  const int len = s.lengths[u];
+  const int t = pos < 0 ? len : pos;
   const bool room = t < s.max_pages * P;
   const size_t pid = room ? (size_t)s.page_table[(size_t)u * s.max_pages + t / P] : 0;
   __shared__ int s_bad;
@@ -43,6 +46,10 @@ __global__ void __launch_bounds__(D) append_token_kernel(akv_store_t s, const ui
   }
   if (!room) {
     if (c == 0 && status[u] == 0) status[u] = status_word(AKV_STATUS_CAPACITY, t);
+    return;
+  }
+  if (t > len) {
+    if (c == 0 && status[u] == 0) status[u] = status_word(AKV_STATUS_POSITION, t);
     return;
   }
   const int tt = t % P;
@@ -545,12 +552,22 @@ extern "C" int akv_append(const akv_store_t* store, const uint16_t* k, const uin
   if (n_new == 0 || store->n_units == 0) return AKV_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_new == 1) {
-    launch_pdl(append_token_kernel, dim3(store->n_units), dim3(D), 0, st, *store, k, v, status);
+    launch_pdl(PDL_APPEND, append_token_kernel, dim3(store->n_units), dim3(D), 0, st, *store, k, v, status, -1);
   } else {
     append_validate_kernel<<<store->n_units, 256, 0, st>>>(*store, k, v, n_new, status);
     const int chunks = (n_new + P - 1) / P + 1;
     append_bulk_kernel<<<dim3(chunks, store->n_units), 256, 0, st>>>(*store, k, v, n_new, status);
     append_commit_kernel<<<(store->n_units + 127) / 128, 128, 0, st>>>(*store, n_new, status);
   }
+  return cudaGetLastError() == cudaSuccess ? AKV_OK : AKV_ECUDA;
+}
+
+extern "C" int akv_append_at(const akv_store_t* store, const uint16_t* k, const uint16_t* v, int32_t pos,
+                             int64_t* status, void* stream) {
+  if (!store || !k || !v || !status || pos < 0) return AKV_EINVAL;
+  if (store->head_dim != D) return AKV_EUNSUPPORTED;
+  if (store->n_units == 0) return AKV_OK;
+  launch_pdl(PDL_APPEND, append_token_kernel, dim3(store->n_units), dim3(D), 0, (cudaStream_t)stream, *store, k, v,
+             status, pos);
   return cudaGetLastError() == cudaSuccess ? AKV_OK : AKV_ECUDA;
 }

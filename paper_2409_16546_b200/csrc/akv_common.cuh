@@ -219,9 +219,18 @@ __device__ __forceinline__ size_t unit_page(const UnitPages& f, const akv_store_
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Kernel classes of the decode chain.  AKV_NOPDL (bit mask of classes, A/B probes) launches
+// those classes without programmatic stream serialization.
+enum { PDL_APPEND = 0, PDL_QK = 1, PDL_SELECT = 2, PDL_PV = 3, PDL_COMBINE = 4 };
+inline int env_int(const char* name, int dflt);
+inline int nopdl_mask() {
+  static const int m = env_int("AKV_NOPDL", 1 << PDL_APPEND);
+  return m;
+}
+
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                              Args... args) {
+inline cudaError_t launch_pdl(int cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = grid;
   lc.blockDim = block;
@@ -231,7 +240,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
+  lc.numAttrs = (nopdl_mask() >> cls) & 1 ? 0 : 1;
   return cudaLaunchKernelEx(&lc, kernel, args...);
 }
 

@@ -780,7 +780,7 @@ static void launch_pv3_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg * S::NPASS;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
-  launch_pdl(pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg);
+  launch_pdl(PDL_PV, pv3_kernel<G, TRUNC, EXPORT, UNIFORM>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg);
 }
 
 }  // namespace akv
@@ -850,7 +850,7 @@ void launch_pv(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st,
 }
 
 void launch_combine(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t& st, cudaStream_t stream) {
-  launch_pdl(combine_kernel, dim3(s.n_units * cfg.group), dim3(D), 0, stream, s, cfg, st);
+  launch_pdl(PDL_COMBINE, combine_kernel, dim3(s.n_units * cfg.group), dim3(D), 0, stream, s, cfg, st);
 }
 
 }  // namespace akv

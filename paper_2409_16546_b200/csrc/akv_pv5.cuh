@@ -441,7 +441,7 @@ static bool launch_pv5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
-  launch_pdl(pv5_kernel<G>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg, tm);
+  launch_pdl(PDL_PV, pv5_kernel<G>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg, tm);
   return true;
 }
 

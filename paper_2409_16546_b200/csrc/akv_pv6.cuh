@@ -649,7 +649,7 @@ static bool launch_pv6_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
-  launch_pdl(pv6_kernel<G, EXPORT>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg, tm,
+  launch_pdl(PDL_PV, pv6_kernel<G, EXPORT>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg, tm,
              tp, ts, tn);
   return true;
 }

@@ -473,7 +473,7 @@ static void launch_qk8_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const long long items = (long long)s.n_units * npg;
   const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
   const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
-  launch_pdl(qk8_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
+  launch_pdl(PDL_QK, qk8_kernel<G, TRUNC>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd, npg);
 }
 
 }  // namespace akv

@@ -477,9 +477,9 @@ void launch_select(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t&
   // long contexts: more threads per head (the per-head chain is the latency); 512 threads
   // keep 2 CTAs per SM, so up to 296 heads run in one wave (c4: 1024 threads 47 us, 512: 43 us)
   if (max_len > 8192)
-    launch_pdl(select_kernel<512>, dim3(s.n_units * cfg.group), dim3(512), 0, stream, s, cfg, st, cap);
+    launch_pdl(PDL_SELECT, select_kernel<512>, dim3(s.n_units * cfg.group), dim3(512), 0, stream, s, cfg, st, cap);
   else
-    launch_pdl(select_kernel<256>, dim3(s.n_units * cfg.group), dim3(256), 0, stream, s, cfg, st, cap);
+    launch_pdl(PDL_SELECT, select_kernel<256>, dim3(s.n_units * cfg.group), dim3(256), 0, stream, s, cfg, st, cap);
 }
 
 }  // namespace akv

@@ -523,3 +523,45 @@ def test_metered_reads_match_oracle():
             c.ostore(1).read_element(c.ostore(1).k if which == "k" else c.ostore(1).v, 599, 127, 12, OCounter())
     with pytest.raises(IndexError):
         c.store.read_element(0, 0, 600, 0, 8, AccessCounter())
+
+
+def test_append_at_truncates_and_appends():
+    """akv_append_at (include/akv.h): truncate to pos and append there; pos beyond the length
+    is rejected with AKV_STATUS_POSITION and leaves the unit unchanged."""
+    import ctypes
+
+    from paper_2409_16546_b200 import _lib
+
+    c = Case(B=1, Hkv=2, n=300, seed=31)
+    st, L = c.store, _lib.lib()
+    K2, V2, _ = generate_batch(1, 2, 1, 128, 1, 77)
+    k = torch.from_numpy(K2.view(np.int16)).view(1, 2, 128).cuda()
+    v = torch.from_numpy(V2.view(np.int16)).view(1, 2, 128).cuda()
+    st.status_dev.zero_()
+    _lib.check(L.akv_append_at(ctypes.byref(st.c_store), k.data_ptr(), v.data_ptr(), 297, st.status_dev.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream), "akv_append_at")
+    torch.cuda.synchronize()
+    assert (st.lengths_dev.cpu() == 298).all() and not st.status_dev.cpu().any()
+    st._host_len[:] = 298
+    cm_before = c.store.colmax().cpu().numpy()
+    for which, src, new in (("k", c.K, K2), ("v", c.V, V2)):
+        p0, p1, p2 = st.export_planes(which)
+        for u in range(2):
+            words = np.concatenate([src[u][:297], new[u][:1]])
+            ref = OPlane.from_words(words)
+            assert np.array_equal(p0[0, u][:298], ref.plane0)
+            assert np.array_equal(p1[0, u][:298], ref.plane1)
+            assert np.array_equal(p2[0, u][:298], ref.plane2)
+    # ColMax is the running max over every appended token (the truncated ones included)
+    for u in range(2):
+        o = c.ostore(u)
+        want = np.maximum(o.colmax, (K2[u][0] & 0x7FFF).astype(np.uint16))
+        assert np.array_equal(cm_before[0, u].astype(np.uint16), want)
+    # beyond the length: rejected, unchanged
+    st.status_dev.zero_()
+    _lib.check(L.akv_append_at(ctypes.byref(st.c_store), k.data_ptr(), v.data_ptr(), 299, st.status_dev.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream), "akv_append_at")
+    torch.cuda.synchronize()
+    s = st.status_dev.cpu().numpy()
+    assert all((int(w) >> 60) == _lib.STATUS_POSITION for w in s)
+    assert (st.lengths_dev.cpu() == 298).all()
