@@ -105,6 +105,13 @@ __device__ __forceinline__ uint4 ld_stream_u128(const void* p, uint64_t pol) {
 // mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// One elected lane of a converged warp (elect.sync): warp-uniform operands of the elected
+// lane's TMA / MMA issue stay in uniform registers (no per-lane R2UR waterfall).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
   };
   auto meta_issue = [&](int u, int pg, int slot) {
     meta_wait(slot);  // a slot is re-armed only after its previous phase completed
-    if (lane == 0) {
+    if (elect_one()) {
       uint32_t* dst = metab + slot * MW;
       mbar_arrive_expect_tx(&mbar[slot], 96 * G);
       tma_load_2d(dst, &tms, pg * 8, u * G, &mbar[slot]);                             // sel words of the G heads
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
     const int slot = kiss % MAXS;
     uint8_t* dst = ring + off;
     const uint8_t* vb = s.v_pool + ic.pid * PAGE;
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_arrive_expect_tx(&sbar[slot], S::HEAD + 64 * (nm + nl) + S::PB);
       tma_load_2d(dst, &tmv, 0, (int)(ic.pid * 512 + r0), &sbar[slot]);
       tma_load_2d(pblk + slot * G * R, &tmp, ic.pg * P + r0, ic.u * G, &sbar[slot]);  // p of the G heads
