@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(32 * Pv6Shape<G>::WARPS, Pv6Shape<G>::MINB)
     const int size = pv6_stage_bytes(nm, nl);
     const int off = ioff + size > RING ? 0 : ioff;
     const int need = size + (off == ioff ? 0 : RING - ioff);
-    if (used + need > RING) return false;
+    if (used > 0 && used + need > RING) return false;  // an empty ring takes any stage (<= RING)
     const int slot = kiss % MAXS;
     uint8_t* dst = ring + off;
     const uint8_t* vb = s.v_pool + ic.pid * PAGE;
