@@ -420,7 +420,7 @@ static void launch_pv4_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int cap = s.max_pages * P;
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  const int grid = balanced_grid(items, resident, S::WARPS);
   launch_pdl(PDL_PV, pv4_kernel<G, TRUNC, EXPORT, UNIFORM>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg,
              st, cap, npg);
 }

@@ -648,7 +648,7 @@ static bool launch_pv6_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
   const int resident = resident_ctas<pv6_kernel<G, EXPORT>>(32 * S::WARPS, S::SMEM);
   const int npg = (max_len + P - 1) / P;
   const long long items = (long long)s.n_units * npg;
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  const int grid = balanced_grid(items, resident, S::WARPS, G <= 2);  // G = 4: fewer warps cost more (c3)
   launch_pdl(PDL_PV, pv6_kernel<G, EXPORT>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, npg, tm,
              tp, ts, tn);
   return true;

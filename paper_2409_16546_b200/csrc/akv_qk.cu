@@ -1078,7 +1078,7 @@ static void launch_qk5_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_s
     return;
   }
   const int resident = resident_ctas<qk5_kernel<G, TRUNC, false>>(32 * S::WARPS, S::SMEM);
-  const int grid = (int)std::min<long long>(resident, std::max<long long>((items + S::WARPS - 1) / S::WARPS, 1));
+  const int grid = balanced_grid(items, resident, S::WARPS);
   launch_pdl(PDL_QK, qk5_kernel<G, TRUNC, false>, dim3(grid), dim3(32 * S::WARPS), (size_t)S::SMEM, stream, s, cfg, st, cap, isd,
              npg, t256, t128);
 }
@@ -1114,7 +1114,7 @@ static void launch_qk_t(const akv_store_t& s, const akv_cfg_t& cfg, const akv_st
     const int cap = s.max_pages * P;
     const int npg = (max_len + P - 1) / P;
     const long long items = (long long)s.n_units * npg;
-    const int grid = (int)std::min<long long>(resident, std::max<long long>((items + QK_WARPS - 1) / QK_WARPS, 1));
+    const int grid = balanced_grid(items, resident, QK_WARPS);
     const float isd = (float)(1.0 / 11.313708498984761);  // 1/sqrt(128)
     launch_pdl(PDL_QK, qk_kernel<G, TRUNC>, dim3(grid), dim3(32 * QK_WARPS), smem, stream, s, cfg, st, cap, isd, npg);
   }
