@@ -80,13 +80,6 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-// L2 evict-last: a unit's last K page, which the next step's append rewrites (partial-sector
-// writes into channel-major rows hit L2 instead of reading DRAM) and its qk reads again.
-__device__ __forceinline__ uint64_t evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ uint2 ld_stream_u64(const void* p, uint64_t pol) {
   uint2 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"

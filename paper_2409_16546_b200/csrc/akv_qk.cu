@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
   QkWarp<G>& ws = reinterpret_cast<QkWarp<G>*>(qk_smem_raw)[warp];
   if (lane == 0) ws.unit = -1;
   __syncwarp();
-  const uint64_t pol_first = evict_first_policy(), pol_last = evict_last_policy();
+  const uint64_t pol = evict_first_policy();
   uint32_t tkm = 0xFFFFFFFFu, tf = 0u;
   if (TRUNC) {
     const int kb = cfg.trunc_bits - 6;
@@ -420,7 +420,6 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
     if (ws.unit != u || pg == 0) k_prologue<G, TRUNC>(ws, s, cfg, st, u, n, pg == 0);
     const uint8_t* base = s.k_pool + unit_page(up, s, pg) * PAGE;
     const int nb8 = ws.n8p >> 3, nb = ws.nlist >> 3;
-    const uint64_t pol = (pg + 1) * P >= n ? pol_last : pol_first;  // the unit's last page stays in L2
 
 #pragma unroll 1
     for (int j0 = 0; j0 < G; j0 += HG) {
