@@ -247,6 +247,27 @@ class KVStore:
             raise ValueError(f"append beyond capacity at batch {b}, kv-head {h}")
         raise ValueError(f"append failed with status 0x{int(st[u]):016X}")
 
+    def append_token_at(self, pos: int, k_row, v_row) -> None:
+        """Truncate every unit to `pos` tokens and append one token there (akv_append_at: one
+        launch; speculative rollback, fixed-context replay).  pos must not exceed any unit's
+        length.  ColMax keeps its running max over every token ever appended."""
+        k = self._shape_rows(k_row, "k")
+        v = self._shape_rows(v_row, "v")
+        if k.shape != v.shape or int(k.shape[2]) != 1:
+            raise ValueError("append_token_at takes one k row and one v row per unit")
+        if not 0 <= pos <= int(self._host_len.min()):
+            raise ValueError(f"position {pos} outside [0, {int(self._host_len.min())}]")
+        if pos + 1 > self.capacity:
+            raise ValueError(f"append at {pos} exceeds capacity {self.capacity}")
+        self.status_dev.zero_()
+        _lib.check(self._L.akv_append_at(ctypes.byref(self.c_store), k.data_ptr(), v.data_ptr(), int(pos),
+                                         self.status_dev.data_ptr(), self._stream()), "akv_append_at")
+        before = np.full_like(self._host_len, pos)
+        self._host_len[:] = pos + 1
+        self._pending = (k, v, before, 1)
+        if self.strict:
+            self.check()
+
     def rewind(self, n_tokens: int) -> None:
         """Set every unit's length to n_tokens (<= current).  ColMax keeps its running max."""
         if n_tokens > int(self._host_len.min()):

@@ -565,3 +565,20 @@ def test_append_at_truncates_and_appends():
     s = st.status_dev.cpu().numpy()
     assert all((int(w) >> 60) == _lib.STATUS_POSITION for w in s)
     assert (st.lengths_dev.cpu() == 298).all()
+
+
+def test_append_token_at_api_matches_fresh_store():
+    """KVStore.append_token_at: truncate to pos and append through the Python API (the planes
+    hold the first pos tokens plus the new one); a position beyond the length is rejected."""
+    c = Case(B=1, Hkv=2, n=300, seed=41)
+    K2, V2, _ = generate_batch(1, 2, 1, 128, 1, 42)
+    k = torch.from_numpy(K2.view(np.int16)).view(1, 2, 128)
+    v = torch.from_numpy(V2.view(np.int16)).view(1, 2, 128)
+    c.store.append_token_at(250, k, v)
+    assert (c.store.lengths == 251).all()
+    p0, _, _ = c.store.export_planes("k")
+    for u in range(2):
+        ref = OPlane.from_words(np.concatenate([c.K[u][:250], K2[u][:1]]))
+        assert np.array_equal(p0[0, u][:251], ref.plane0)
+    with pytest.raises(ValueError):
+        c.store.append_token_at(300, k, v)
