@@ -32,7 +32,7 @@ tail -1 gpurun_out/b_c5.log | cut -c1-400
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-validate > gpurun_out/launches_bench.log 2>&1
 echo "launches rc=$?"
-timeout 900 ncu -f --set full --import-source on --clock-control none -k regex:"qk_kernel|select_kernel|pv6_kernel|pv5_kernel|pv3_kernel|append_token|combine" -c 5 \
+timeout 900 ncu -f --set full --import-source on --clock-control none -k regex:"qk_kernel|select_kernel|pv6_kernel|append_token|combine" -c 5 \
   -o /tmp/prof_c2 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-validate > gpurun_out/prof_bench.log 2>&1
 echo "ncu rc=$?"
 ncu -i /tmp/prof_c2.ncu-rep --page raw --csv > gpurun_out/prof_c2_raw.csv 2>&1
