@@ -494,26 +494,42 @@ __global__ void __launch_bounds__(32 * QK_WARPS, QkShape<G>::MINB) qk_kernel(akv
 // 128 B per LDS.128; the 128 B nibble rows are stored with their 64 B halves
 // swapped on every other row pair.
 // ---------------------------------------------------------------------------
+#ifndef AKV_QK5_NB4
+#define AKV_QK5_NB4 3
+#endif
+#ifndef AKV_QK5_MINB4
+#define AKV_QK5_MINB4 3
+#endif
 constexpr int Q5_SLOT = 4096;
 constexpr int Q5_CHUNKS = 18;  // (128 + 15 + 7) / 8 eight-channel chunks: T8 class padded to 16, T12/T16 class to 8
 
 template <int G>
 struct alignas(16) Qk5Warp {
   uint32_t off[Q5_CHUNKS * 8];            // list position -> channel * P
-  uint32_t bf[Q5_CHUNKS][3][32];          // per chunk, tier variant (T8, T12, T16), lane: the B fragment
+  // per chunk, tier variant (T8, T12, T16), lane (g, t): the B fragment; G <= 4 keeps only
+  // the lanes of heads g < 4 (lanes 0..15; the padding heads' fragments are zero)
+  uint32_t bf[Q5_CHUNKS][3][G <= 4 ? 16 : 32];
   uint32_t low[(Q5_CHUNKS * 8 + 31) / 32];  // list position bitmask: low row needed (T16 in the union)
   uint8_t vmask[Q5_CHUNKS];               // variants present per chunk (bit 0 T8, 1 T12, 2 T16)
   int n8p, nlp, unit, pad;
 };
 
 template <int G>
+__device__ __forceinline__ uint32_t q5_bfrag(const Qk5Warp<G>& ws, int c, int v) {
+  const int lane = threadIdx.x & 31;
+  if (G <= 4) return lane < 16 ? ws.bf[c][v][lane] : 0u;
+  return ws.bf[c][v][lane];
+}
+
+template <int G>
 struct Qk5Shape {
   static constexpr int WARPS = 4;
-  static constexpr int NB = 5;  // ring slots per warp
+  // G = 4: 3 ring slots and 168 registers -> 3 CTAs (12 warps) per SM; G = 8: 5 slots, 2 CTAs
+  static constexpr int NB = G <= 4 ? AKV_QK5_NB4 : 5;  // ring slots per warp
   static constexpr int LIST = (sizeof(Qk5Warp<G>) + 127) & ~127;
   static constexpr int PER_WARP = LIST + NB * Q5_SLOT + 128;  // list | ring | slot mbarriers (TMA staging)
   static constexpr int SMEM = WARPS * PER_WARP;
-  static constexpr int MINB = 2;
+  static constexpr int MINB = G <= 4 ? AKV_QK5_MINB4 : 2;
   static_assert(G * Q5_CHUNKS * 8 * 3 <= NB * Q5_SLOT, "prologue scratch must fit the ring");
 };
 
@@ -594,7 +610,7 @@ __device__ void k5_prologue(Qk5Warp<G>& ws, uint8_t* scratch, const akv_store_t&
     for (int v = 0; v < 3; ++v) {
       const uint32_t tier = 8u + 4u * v;
       const uint32_t b = (c0 == tier ? q0 : 0u) | ((c1 == tier ? q1 : 0u) << 16);
-      ws.bf[c][v][lane] = b;
+      if (G > 4 || lane < 16) ws.bf[c][v][lane & (G <= 4 ? 15 : 31)] = b;
       if (__any_sync(0xFFFFFFFFu, b != 0u)) vm |= 1u << v;
     }
     if (lane == 0) ws.vmask[c] = (uint8_t)(c < n8c ? 1u : vm);
@@ -784,7 +800,7 @@ __device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
           X.h[j][hf] = *reinterpret_cast<const uint4*>(slot + (8 * cc + 2 * t + j) * 256 + 128 * hf + 16 * g);
-      k5_compute_t8(X, ws.bf[2 * b + cc][0][lane], acc, c80);
+      k5_compute_t8(X, q5_bfrag<G>(ws, 2 * b + cc, 0), acc, c80);
     }
   } else {
     const int ch = (ws.n8p >> 3) + (b - n8s), p0 = ws.n8p + 8 * (b - n8s) + 2 * t;
@@ -803,7 +819,7 @@ __device__ __forceinline__ void q5_compute(const uint8_t* slot, const Qk5Warp<G>
                                         : make_uint2(0x88888888u, 0x88888888u);
       }
     }
-    const uint32_t b8 = ws.bf[ch][0][lane], b12 = ws.bf[ch][1][lane], b16 = ws.bf[ch][2][lane];
+    const uint32_t b8 = q5_bfrag<G>(ws, ch, 0), b12 = q5_bfrag<G>(ws, ch, 1), b16 = q5_bfrag<G>(ws, ch, 2);
     k5_compute_full<TRUNC>(X, N, ws.vmask[ch], b8, b12, b16, acc, tkm, tf, c80);
   }
 }
