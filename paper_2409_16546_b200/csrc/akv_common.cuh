@@ -229,7 +229,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // Kernel classes of the decode chain.  AKV_NOPDL (bit mask of classes, A/B probes) launches
 // those classes without programmatic stream serialization.
-enum { PDL_APPEND = 0, PDL_QK = 1, PDL_SELECT = 2, PDL_PV = 3, PDL_COMBINE = 4 };
+enum { PDL_APPEND = 0, PDL_QK = 1, PDL_SELECT = 2, PDL_PV = 3, PDL_COMBINE = 4, PDL_OFF = 30 };
 inline int env_int(const char* name, int dflt);
 inline int nopdl_mask() {
   static const int m = env_int("AKV_NOPDL", 1 << PDL_APPEND);
@@ -248,7 +248,7 @@ inline cudaError_t launch_pdl(int cls, void (*kernel)(KArgs...), dim3 grid, dim3
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = (nopdl_mask() >> cls) & 1 ? 0 : 1;
+  lc.numAttrs = (cls == PDL_OFF || ((nopdl_mask() >> cls) & 1)) ? 0 : 1;
   return cudaLaunchKernelEx(&lc, kernel, args...);
 }
 

@@ -476,10 +476,17 @@ void launch_select(const akv_store_t& s, const akv_cfg_t& cfg, const akv_step_t&
   const int cap = s.max_pages * P;
   // long contexts: more threads per head (the per-head chain is the latency); 512 threads
   // keep 2 CTAs per SM, so up to 296 heads run in one wave (c4: 1024 threads 47 us, 512: 43 us)
-  if (max_len > 8192)
-    launch_pdl(PDL_SELECT, select_kernel<512>, dim3(s.n_units * cfg.group), dim3(512), 0, stream, s, cfg, st, cap);
-  else
-    launch_pdl(PDL_SELECT, select_kernel<256>, dim3(s.n_units * cfg.group), dim3(256), 0, stream, s, cfg, st, cap);
+  // a grid of more than one wave is launched without PDL: early-launched CTAs of the first wave
+  // squat on SMs through the previous kernel's tail and the second wave starts late (c3, 1024
+  // heads over 592 slots: 256.5 -> 239.5 us per step; one-wave grids keep PDL: c2 144.1 vs 145.7)
+  const int heads = s.n_units * cfg.group;
+  if (max_len > 8192) {
+    const int res = resident_ctas<select_kernel<512>>(512, 0);
+    launch_pdl(heads > res ? PDL_OFF : PDL_SELECT, select_kernel<512>, dim3(heads), dim3(512), 0, stream, s, cfg, st, cap);
+  } else {
+    const int res = resident_ctas<select_kernel<256>>(256, 0);
+    launch_pdl(heads > res ? PDL_OFF : PDL_SELECT, select_kernel<256>, dim3(heads), dim3(256), 0, stream, s, cfg, st, cap);
+  }
 }
 
 }  // namespace akv
